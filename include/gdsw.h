@@ -1,0 +1,216 @@
+/*
+ * gdsw.h — C ABI of libgdsw.so, the B200 (sm_100a) solve path of the
+ * two-level rGDSW Schwarz preconditioner with single-reduce GMRES.
+ *
+ * This is the drop-in boundary. The reference (schwarzdd, pure Python) has
+ * no FFI of its own; its boundary is the Python duck-typed interface listed
+ * next to each entry point below. A caller binds these with ctypes
+ * (see INTEGRATION.md); paper_2304_04876_b200/device.py is that binding.
+ *
+ * Conventions
+ *  - every entry point returns an int status (GDSW_OK = 0); on failure the
+ *    message is in gdsw_last_error() (thread-local) and the status names the
+ *    Python exception the reference raises for the same condition;
+ *  - vectors passed to apply / spmv / gmres are caller-owned DEVICE
+ *    pointers; setup descriptors carry HOST arrays (int64 like the
+ *    reference's index maps, float64 values) that the library copies;
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream); all work of
+ *    a call is enqueued on it, setup calls synchronize before returning;
+ *  - dtype: GDSW_F64 or GDSW_F32 (the reference's "double"/"single"
+ *    preconditioner precision, schwarz.py:57-73).
+ */
+#ifndef GDSW_H
+#define GDSW_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GDSW_ABI_VERSION 1
+
+enum gdsw_status {
+  GDSW_OK = 0,
+  GDSW_E_VALUE = 1,  /* ValueError            (schwarz.py:297-298, 219-221, 243-245) */
+  GDSW_E_LINALG = 2, /* numpy.linalg.LinAlgError (local_solvers.py:320-324)        */
+  GDSW_E_FLOAT = 3,  /* FloatingPointError    (local_solvers.py:389-394)           */
+  GDSW_E_ARITH = 4,  /* ArithmeticError       (coarse_space.py:198-202)            */
+  GDSW_E_CUDA = 5,   /* RuntimeError: driver / launch failure                      */
+  GDSW_E_TYPE = 6    /* TypeError             (krylov.py:88-100)                   */
+};
+enum gdsw_dtype { GDSW_F64 = 0, GDSW_F32 = 1 };
+enum gdsw_method { GDSW_EXACT_LU = 0, GDSW_ILU_K = 1, GDSW_FAST_ILU = 2 };
+enum gdsw_variant { GDSW_CLASSIC = 0, GDSW_SINGLE_REDUCE = 1 };
+enum gdsw_orth { GDSW_MGS = 0, GDSW_CGS2 = 1 };
+
+typedef struct gdsw_csr gdsw_csr;
+typedef struct gdsw_plan gdsw_plan;
+typedef struct gdsw_precond gdsw_precond;
+typedef struct gdsw_workspace gdsw_workspace;
+
+const char* gdsw_last_error(void);
+int gdsw_abi_version(void);
+
+/* ------------------------------------------------------------------------
+ * Device CSR operator.
+ * Replaces CsrMatrix + spmv / __matmul__ (sparse_core.py:41-82, 117-131,
+ * 186-204; _kernels.py:23-31). Stored as SELL-32; y = alpha*A x + beta*y in
+ * the matrix element type, rows accumulated in column order (bit-identical
+ * to the reference loop).
+ * ---------------------------------------------------------------------- */
+int gdsw_csr_create(gdsw_csr** out, int64_t nrows, int64_t ncols, const int64_t* row_ptr,
+                    const int64_t* col_idx, const void* values, int dtype);
+int gdsw_csr_set_values(gdsw_csr* a, const void* values); /* same pattern refill */
+int gdsw_csr_spmv(const gdsw_csr* a, const void* x, void* y, double alpha, double beta,
+                  void* stream);
+int gdsw_csr_destroy(gdsw_csr* a);
+
+/* ------------------------------------------------------------------------
+ * Symbolic plan = PreconditionerSkeleton (schwarz.py:84-99, 147-203) in the
+ * batched-subdomain device layout: concatenated overlap maps with the
+ * orderings folded in, factor patterns, level schedules, the FastILU
+ * product plan, the owner-computes scatter map and the coarse structure.
+ * Pattern-only; shared by every preconditioner built on it.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int64_t n;          /* vector length */
+  int32_t n_sub;
+  int32_t method;     /* gdsw_method */
+  int64_t n_loc;      /* sum of overlapped block sizes (N_Omega) */
+  const int64_t* sub_ptr;   /* [n_sub+1] block row offsets                      */
+  const int64_t* gmap;      /* [n_loc] global dof of block row k: dofs_i[perm_i[k]] */
+  const int64_t* l_ptr;     /* [n_loc+1] concatenated strict-L rows             */
+  const int64_t* l_idx;     /* block-local column                               */
+  const int64_t* u_ptr;     /* [n_loc+1] concatenated U rows, diagonal first    */
+  const int64_t* u_idx;
+  const int64_t* llev_sub;  /* [n_sub+1] offsets into llev_ptr                  */
+  const int64_t* llev_ptr;  /* [levels+1] offsets into llev_rows                */
+  const int64_t* llev_rows; /* [n_loc] block-local row ids                      */
+  const int64_t* ulev_sub;
+  const int64_t* ulev_ptr;
+  const int64_t* ulev_rows;
+  /* FastILU product plan (method == GDSW_FAST_ILU), concatenated positions */
+  const int64_t* a_of;      /* [nnz_l+nnz_u] A.values index of the entry, -1 = fill */
+  const int64_t* fi_ptr;    /* [nnz_l+nnz_u+1]                                  */
+  const int64_t* fi_pl;     /* L position of each product                       */
+  const int64_t* fi_pu;     /* U position of each product                       */
+  int64_t n_res;            /* residual terms = block-A entries                 */
+  const int64_t* res_sub_ptr; /* [n_sub+1]                                      */
+  const int64_t* res_a;     /* [n_res] A.values index                           */
+  const int64_t* res_ptr;   /* [n_res+1]                                        */
+  const int64_t* res_pl;
+  const int64_t* res_pu;
+  const int64_t* res_tl;    /* -1 when the tail term is a U entry               */
+  const int64_t* res_tu;
+} gdsw_local_desc;
+
+typedef struct {
+  int32_t n_c;              /* coarse dimension                                 */
+  int64_t n_gamma;
+  const int64_t* gamma_rows; /* [n_gamma] sorted interface dofs                 */
+  const int64_t* pg_ptr;    /* [n_gamma+1] Phi rows on the interface            */
+  const int64_t* pg_col;
+  const double* pg_val;     /* copied bitwise from the scaled null space        */
+  const int64_t* int_ptr;   /* [n_sub+1] interior rows per subdomain            */
+  const int64_t* int_rows;
+  const int64_t* col_ptr;   /* [n_sub+1] coarse columns touching each interior  */
+  const int64_t* col_ids;
+  const int64_t* aii_ptr;   /* [n_int+1] A_{I_s I_s}, local interior columns    */
+  const int64_t* aii_col;
+  const int64_t* aii_src;   /* A.values index                                   */
+  const int64_t* aig_ptr;   /* [n_int+1] A_{I_s Gamma}, gamma positions         */
+  const int64_t* aig_col;
+  const int64_t* aig_src;
+} gdsw_coarse_desc;
+
+int gdsw_plan_create(gdsw_plan** out, const gdsw_local_desc* local);
+int gdsw_plan_destroy(gdsw_plan* p);
+
+/* ------------------------------------------------------------------------
+ * Numeric preconditioner = TwoLevelPreconditioner (schwarz.py:130-144,
+ * 213-287). Values live in one device arena per preconditioner.
+ * ---------------------------------------------------------------------- */
+int gdsw_precond_create(gdsw_precond** out, gdsw_plan* plan, int dtype, int trisolve_iters);
+/* coarse structure of this preconditioner: the kept null-space columns per
+ * interface component are value-dependent (interface_basis,
+ * coarse_space.py:64-103), so the coarse pattern is bound in the numeric
+ * phase, like the reference */
+int gdsw_precond_set_coarse(gdsw_precond* m, const gdsw_coarse_desc* coarse);
+/* host-computed exact / ILU(k) factors (build_numeric, local_solvers.py:454-460) */
+int gdsw_precond_set_factors(gdsw_precond* m, const void* l_vals, const void* u_vals);
+/* FastILU sweeps on the GPU (fast_ilu_numeric, local_solvers.py:343-397);
+ * residuals[sweep * n_sub + s] receives the per-sweep nonlinear residuals */
+int gdsw_precond_fastilu(gdsw_precond* m, const gdsw_csr* a, int sweeps, double* residuals);
+int gdsw_precond_get_factors(const gdsw_precond* m, void* l_vals, void* u_vals);
+/* harmonic extension on the GPU (harmonic_extension, coarse_space.py:130-179);
+ * a = the f64 operator the coarse basis is built from; col_resid[K] gets the
+ * max |A_II phi_I + A_IG phi_G| per panel column */
+int gdsw_precond_extend(gdsw_precond* m, const gdsw_csr* a, double tol, int max_iters,
+                        int* iters_out, double* col_resid);
+int64_t gdsw_precond_panel_entries(const gdsw_precond* m);
+int gdsw_precond_get_panels(const gdsw_precond* m, double* panels);
+/* dense A0^-1 (n_c x n_c, row-major, float64; cast to the precond dtype) */
+int gdsw_precond_set_coarse_inverse(gdsw_precond* m, const double* a0inv);
+/* z = Phi A0^-1 Phi^T r + sum_i R_i^T A_i^-1 R_i r  (apply, schwarz.py:290-327) */
+int gdsw_precond_apply(gdsw_precond* m, const double* r, double* z, void* stream);
+/* per-block solves only: y[k] (dtype, concatenated block rows, permuted) =
+ * LocalFactorization.solve of the gathered block (local_solvers.py:263-278);
+ * jacobi_iters > 0 forces FastSpTRSV with that many iterates */
+int gdsw_precond_local_solve(gdsw_precond* m, const double* r, void* y, int jacobi_iters,
+                             void* stream);
+int gdsw_precond_destroy(gdsw_precond* m);
+
+/* ------------------------------------------------------------------------
+ * Right-preconditioned restarted GMRES (gmres, krylov.py:141-161;
+ * _gmres_single_reduce 260-361; _gmres_classic 179-257). The loop runs on
+ * the host in C++; vectors, operator, preconditioner and the fused
+ * reductions on the device. One device->host transfer per iteration carries
+ * the 2(j+1) reduced scalars for the Givens update.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int32_t restart;
+  double rel_tol;
+  int32_t max_iters;
+  int32_t variant;           /* gdsw_variant */
+  int32_t orthogonalization; /* gdsw_orth    */
+} gdsw_krylov_cfg;
+
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  int32_t reduction_count;
+  int32_t iteration_reductions;
+  int32_t residual_reductions;
+  int32_t restarts;
+  int32_t n_history;  /* entries written to history  */
+  int32_t n_true;     /* entries written to true_it / true_res */
+} gdsw_solve_report;
+
+int gdsw_workspace_create(gdsw_workspace** out, int64_t n, int32_t restart);
+int gdsw_workspace_destroy(gdsw_workspace* ws);
+/* m: preconditioner or NULL; m_csr: CSR preconditioner or NULL (both NULL =
+ * identity). x: device, in = x0, out = solution. history/true_* are host
+ * arrays of capacity `cap`. */
+int gdsw_gmres(const gdsw_csr* a, gdsw_precond* m, const gdsw_csr* m_csr, const double* b,
+               double* x, int x0_nonzero, const gdsw_krylov_cfg* cfg, gdsw_workspace* ws,
+               gdsw_solve_report* rep, double* history, int32_t* true_it, double* true_res,
+               int32_t cap, void* stream);
+
+/* fused single-reduce block reduction [V[:j]; v]^T [v, z] (krylov.py:290-300);
+ * out (host) receives 2(j+1) values: [V.v..., v.v, V.z..., v.z] */
+int gdsw_block_dot(const double* V, int64_t ldv, int32_t j, const double* v, const double* z,
+                   int64_t n, double* out, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Instrumentation: per-phase device time (CUDA events on the launching
+ * stream) accumulated while enabled. names: see gdsw_prof_name().
+ * ---------------------------------------------------------------------- */
+int gdsw_prof_enable(int on);
+int gdsw_prof_reset(void);
+int gdsw_prof_count(void);
+const char* gdsw_prof_name(int k);
+int gdsw_prof_read(int k, double* total_ms, int64_t* launches, double* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

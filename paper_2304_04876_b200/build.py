@@ -64,8 +64,8 @@ def build_cuda(force: bool = False) -> Path:
     out = LIB / "libgdsw.so"
     if force or _stale(out, _deps(CSRC, INCLUDE)):
         _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-              "-shared", "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC,
-              *CUDA_SRC, "-o", out, "-lcudart"])
+              "-Xcompiler", "-ffp-contract=off", "-shared", "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC,
+              *CUDA_SRC, "-o", out, "-lcudart", "-Xlinker", "-rpath,/usr/local/cuda/lib64"])
     return out
 
 

@@ -1,0 +1,85 @@
+// Coarse correction of the two-level apply (schwarz.py:302-306):
+//   u = Phi^T r  ->  v = A0^-1 u  ->  (Phi v fused into k_scatter_prolong)
+//
+// Phi is stored the B200 way: for each subdomain s the
+// interior rows are one dense column-major panel n_I_s x k_s over a shared
+// sorted coarse-column list (no per-entry indices, each panel column is a
+// contiguous, coalesced vector), and the interface rows stay CSR. A0^-1 is a
+// dense replicated n_c x n_c block.
+#pragma once
+#include "common.cuh"
+
+namespace gdsw {
+
+struct RestrictDev {
+  int32_t n_c;
+  const int32_t* colsub;     // [K] subdomain of each panel column
+  const int32_t* col_ptr;    // [n_sub+1]
+  const int64_t* panel_off;  // [n_sub]
+  const int32_t* n_int;      // [n_sub]
+  const int32_t* int_ptr;    // [n_sub+1] offsets into int_rows
+  const int32_t* int_rows;   // interior rows (vector positions), per subdomain sorted
+  const int64_t* pgt_ptr;    // [n_c+1] Phi_Gamma^T, coarse-major
+  const int32_t* pgt_row;    // vector position of the interface row
+  const int32_t* clist_ptr;  // [n_c+1] panel columns that map to coarse column c (ascending s)
+  const int32_t* clist;      // panel column ids
+};
+
+// one CTA per panel column: pdot[col] = sum_row P[col][row] * r[int_rows[row]]
+template <typename T>
+__global__ void __launch_bounds__(256) k_restrict_panels(RestrictDev R, const T* __restrict__ panel,
+                                                         const double* __restrict__ r,
+                                                         T* __restrict__ pdot) {
+  const int32_t col = blockIdx.x;
+  const int32_t s = R.colsub[col];
+  const int32_t c = col - R.col_ptr[s];
+  const int32_t ni = R.n_int[s];
+  const T* pc = panel + R.panel_off[s] + (int64_t)c * ni;
+  const int32_t* rows = R.int_rows + R.int_ptr[s];
+  T acc = T(0);
+  for (int32_t i = threadIdx.x; i < ni; i += blockDim.x)
+    acc += ldg_stream(pc + i) * (T)r[__ldg(rows + i)];
+  __shared__ T red[32];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    T t = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : T(0);
+    t = warp_sum(t);
+    if (threadIdx.x == 0) pdot[col] = t;
+  }
+}
+
+// one warp per coarse column: u[c] = Phi_Gamma^T[c,:] r + sum of its panel dots
+template <typename T>
+__global__ void k_restrict_final(RestrictDev R, const T* __restrict__ pgt_val,
+                                 const double* __restrict__ r, const T* __restrict__ pdot,
+                                 T* __restrict__ u) {
+  const int32_t c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (c >= R.n_c) return;
+  T acc = T(0);
+  for (int64_t p = R.pgt_ptr[c] + lane; p < R.pgt_ptr[c + 1]; p += 32)
+    acc += pgt_val[p] * (T)r[R.pgt_row[p]];
+  acc = warp_sum(acc);
+  if (lane == 0) {
+    for (int32_t t = R.clist_ptr[c]; t < R.clist_ptr[c + 1]; ++t) acc += pdot[R.clist[t]];
+    u[c] = acc;
+  }
+}
+
+// dense replicated coarse solve: v = A0^-1 u, one warp per row
+template <typename T>
+__global__ void k_coarse_gemv(int32_t n_c, const T* __restrict__ ainv, const T* __restrict__ u,
+                              T* __restrict__ v) {
+  const int32_t i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= n_c) return;
+  const T* row = ainv + (int64_t)i * n_c;
+  T acc = T(0);
+  for (int32_t j = lane; j < n_c; j += 32) acc += ldg_stream(row + j) * u[j];
+  acc = warp_sum(acc);
+  if (lane == 0) v[i] = acc;
+}
+
+}  // namespace gdsw

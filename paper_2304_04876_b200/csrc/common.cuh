@@ -1,0 +1,139 @@
+// Common device/host utilities for libgdsw (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace gdsw {
+
+// ---------------------------------------------------------------------------
+// error plumbing: every C entry point converts exceptions into a status code
+// and a thread-local message (include/gdsw.h: GDSW_E*)
+// ---------------------------------------------------------------------------
+enum Status : int {
+  OK = 0,
+  E_VALUE = 1,   // ValueError
+  E_LINALG = 2,  // numpy.linalg.LinAlgError
+  E_FLOAT = 3,   // FloatingPointError
+  E_ARITH = 4,   // ArithmeticError
+  E_CUDA = 5,    // RuntimeError (driver / launch)
+  E_TYPE = 6,    // TypeError
+};
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) ::gdsw::cuda_check((x), #x)
+#define CK_LAUNCH() ::gdsw::cuda_check(cudaGetLastError(), "kernel launch")
+
+inline void require(bool ok, const std::string& msg, int code = E_VALUE) {
+  if (!ok) throw Error(code, msg);
+}
+
+// ---------------------------------------------------------------------------
+// owning device buffer
+// ---------------------------------------------------------------------------
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) CK(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void upload(const T* host, size_t count) {
+    alloc(count);
+    if (count) CK(cudaMemcpy(p, host, count * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  void upload(const std::vector<T>& v) { upload(v.data(), v.size()); }
+  void zero(cudaStream_t s = 0) {
+    if (n) CK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  std::vector<T> download() const {
+    std::vector<T> h(n);
+    if (n) CK(cudaMemcpy(h.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost));
+    return h;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// narrow a host int64 array to int32 with a range check
+inline std::vector<int32_t> to_i32(const int64_t* a, size_t n, int64_t add = 0) {
+  std::vector<int32_t> out(n);
+  for (size_t i = 0; i < n; ++i) {
+    int64_t v = a[i] + add;
+    require(v >= INT32_MIN && v <= INT32_MAX, "index exceeds the int32 device layout");
+    out[i] = (int32_t)v;
+  }
+  return out;
+}
+
+inline int num_sms() {
+  static int sms = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return sms;
+}
+
+inline unsigned grid_for(int64_t work, int block, int64_t cap = 1 << 30) {
+  int64_t g = (work + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (unsigned)g;
+}
+
+// ---------------------------------------------------------------------------
+// IEEE round-to-nearest arithmetic without FMA contraction. The reference's
+// numba loops (_kernels.py:12-16, no fastmath) round every product and sum
+// separately; using these keeps the sequential kernels bit-identical.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double rn_mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float rn_mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double rn_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float rn_add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double rn_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float rn_sub(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double rn_div(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float rn_div(float a, float b) { return __fdiv_rn(a, b); }
+
+// read-only streaming load (values/indices are read once per pass)
+template <typename T>
+__device__ __forceinline__ T ldg_stream(const T* p) { return __ldcs(p); }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace gdsw

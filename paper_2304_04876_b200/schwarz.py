@@ -1,0 +1,449 @@
+"""Two-level additive overlapping Schwarz preconditioner, B200 solve path
+(mirrors schwarzdd.schwarz, schwarz.py:1-327).
+
+    z = Phi A0^-1 Phi^T r + sum_i R_i^T A_i^-1 R_i r
+
+* `setup_symbolic` (host, pattern only; schwarz.py:147-203): overlap maps,
+  orderings, symbolic factorizations and the batched-subdomain device plan
+  (concatenated maps, factor patterns, level schedules, FastILU product
+  lists, the owner-computes scatter map).
+* `setup_numeric` (schwarz.py:213-287): FastILU sweeps and the harmonic
+  extension run on the GPU; exact/ILU(k) numeric factors and the small
+  Galerkin product A0 on the host; dense A0^-1 replicated on the device.
+  Repeatable on the same skeleton (each call returns an independent
+  preconditioner arena).
+* `apply` (schwarz.py:290-327): one call into libgdsw -- coarse restriction,
+  dense coarse solve, batched local solves (FastSpTRSV or level-set SpTRSV,
+  all subdomains per launch), then the scatter fused with the coarse
+  prolongation, contributions summed in fixed subdomain order. Single
+  precision rounds r once, runs in fp32, promotes the result.
+"""
+
+from __future__ import annotations
+
+import hashlib
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _host
+from .coarse_space import (
+    coarse_matrix,
+    extend_on_device,
+    interface_basis,
+    interior_sets as _interior_sets,
+)
+from .decomposition import Decomposition
+from .local_solvers import (
+    LocalFactorization,
+    SolverSpec,
+    build_symbolic,
+    host_numeric,
+    make_ordering,
+    numeric_lu,
+    symbolic_lu,
+)
+from .sparse_core import (
+    CsrMatrix,
+    convert_precision,
+    extract_submatrix,
+    extract_with_source,
+    transpose,
+)
+
+PRECISIONS = ("double", "single")
+_METHOD_CODE = {"exact_lu": 0, "ilu_k": 1, "fast_ilu": 2}
+
+
+@dataclass(frozen=True)
+class SchwarzConfig:
+    local: SolverSpec = SolverSpec()
+    use_coarse: bool = True
+    precision: str = "double"
+    ordering: str = "nested_dissection"
+    threads: int = 1
+
+    def __post_init__(self):
+        if not isinstance(self.local, SolverSpec):
+            raise TypeError("local must be a SolverSpec")
+        if self.precision not in PRECISIONS:
+            raise ValueError(f"unknown precision {self.precision!r}")
+        if self.ordering not in ("natural", "nested_dissection"):
+            raise ValueError(f"unknown ordering kind {self.ordering!r}")
+        if self.threads < 1:
+            raise ValueError("threads must be at least 1")
+
+
+def _pattern_fingerprint(a: CsrMatrix) -> str:
+    h = hashlib.sha256()
+    h.update(np.array([a.nrows, a.ncols], dtype=np.int64).tobytes())
+    h.update(a.row_ptr.tobytes())
+    h.update(a.col_idx.tobytes())
+    return h.hexdigest()
+
+
+# ---------------------------------------------------------------------------
+# device plan assembly (batched-subdomain layout)
+# ---------------------------------------------------------------------------
+
+def _cat(arrays, dtype=np.int64):
+    return np.concatenate(arrays).astype(dtype, copy=False) if arrays else np.zeros(0, dtype)
+
+
+def local_plan_arrays(n: int, sets: list, symbolics: list, method: str, a: CsrMatrix | None,
+                      _unused=None) -> dict:
+    """Concatenate every block's ordering, factor pattern and level schedules
+    into the descriptor of gdsw_plan_create. For fast_ilu, also flatten the
+    fixed-point product lists (gh_fastilu_plan) against A.values positions."""
+    n_sub = len(sets)
+    sizes = np.array([s.size for s in sets], dtype=np.int64)
+    sub_ptr = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    n_loc = int(sub_ptr[-1])
+    gmap = _cat([np.asarray(d, np.int64)[sym.ordering.perm] for d, sym in zip(sets, symbolics)])
+
+    def cat_ptr(ptrs):
+        out, off = [np.zeros(1, dtype=np.int64)], 0
+        for p in ptrs:
+            out.append(p[1:] + off)
+            off += int(p[-1])
+        return np.concatenate(out)
+
+    l_ptr = cat_ptr([s.l_ptr for s in symbolics])
+    u_ptr = cat_ptr([s.u_ptr for s in symbolics])
+    l_idx = _cat([s.l_idx for s in symbolics])
+    u_idx = _cat([s.u_idx for s in symbolics])
+
+    def cat_levels(ptrs, rows):
+        sub = np.concatenate([[0], np.cumsum([p.size - 1 for p in ptrs])]).astype(np.int64)
+        lp = [np.asarray(p[:-1], np.int64) + sub_ptr[s] for s, p in enumerate(ptrs)]
+        return sub, _cat(lp + [np.array([n_loc])]), _cat(rows)
+
+    llev_sub, llev_ptr, llev_rows = cat_levels([s.l_level_ptr for s in symbolics],
+                                               [s.l_level_rows for s in symbolics])
+    ulev_sub, ulev_ptr, ulev_rows = cat_levels([s.u_level_ptr for s in symbolics],
+                                               [s.u_level_rows for s in symbolics])
+    out = dict(n=n, n_sub=n_sub, method=_METHOD_CODE[method], n_loc=n_loc, sub_ptr=sub_ptr,
+               gmap=gmap, l_ptr=l_ptr, l_idx=l_idx, u_ptr=u_ptr, u_idx=u_idx,
+               llev_sub=llev_sub, llev_ptr=llev_ptr, llev_rows=llev_rows, ulev_sub=ulev_sub,
+               ulev_ptr=ulev_ptr, ulev_rows=ulev_rows, n_res=0)
+    if method == "fast_ilu":
+        out.update(_fastilu_arrays(sets, symbolics, a, l_ptr, u_ptr))
+    return out
+
+
+def _fastilu_arrays(sets, symbolics, a: CsrMatrix, l_ptr, u_ptr) -> dict:
+    nnz_l, nnz_u = int(l_ptr[-1]), int(u_ptr[-1])
+    a_of_l, a_of_u, e_l, e_u, pl_l, pu_l, pl_u, pu_u = ([] for _ in range(8))
+    res_sub, res_a, res_ptr_parts, rpl, rpu, rtl, rtu = [0], [], [], [], [], [], []
+    lo = uo = 0
+    epl_off = epu_off = res_off = 0
+    for dofs, sym in zip(sets, symbolics):
+        blk, src = extract_with_source(a, dofs, dofs)
+        perm = sym.ordering.perm
+        inv = np.empty_like(perm)
+        inv[perm] = np.arange(perm.size, dtype=np.int64)
+        p_ptr, p_idx, p_src = _host.csr_gather(blk.row_ptr, blk.col_idx, perm, inv)
+        gsrc = src[p_src]                      # A.values position of each permuted entry
+        al = _host.align_pattern(p_ptr, p_idx, sym.l_ptr, sym.l_idx)
+        au = _host.align_pattern(p_ptr, p_idx, sym.u_ptr, sym.u_idx)
+        a_of_l.append(np.where(al >= 0, gsrc[np.maximum(al, 0)], -1))
+        a_of_u.append(np.where(au >= 0, gsrc[np.maximum(au, 0)], -1))
+        (e_ptr, pl, pu, r_ptr, r_l, r_u, t_l, t_u) = _host.fastilu_plan(
+            sym.n, sym.l_ptr, sym.l_idx, sym.u_ptr, sym.u_idx, p_ptr, p_idx)
+        nl = sym.l_idx.size
+        nlp = int(e_ptr[nl])
+        # L entries: products are pair slices [0, nlp); U entries follow
+        e_l.append(np.diff(e_ptr[:nl + 1]))
+        e_u.append(np.diff(e_ptr[nl:]))
+        pl_l.append(pl[:nlp] + lo)
+        pu_l.append(pu[:nlp] + uo)
+        pl_u.append(pl[nlp:] + lo)
+        pu_u.append(pu[nlp:] + uo)
+        res_a.append(gsrc)
+        res_ptr_parts.append(np.diff(r_ptr))
+        rpl.append(r_l + lo)
+        rpu.append(r_u + uo)
+        rtl.append(np.where(t_l >= 0, t_l + lo, -1))
+        rtu.append(t_u + uo)
+        res_sub.append(res_sub[-1] + gsrc.size)
+        lo += nl
+        uo += sym.u_idx.size
+    counts = np.concatenate(e_l + e_u)
+    fi_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    rcounts = _cat(res_ptr_parts)
+    return dict(a_of=_cat(a_of_l + a_of_u), fi_ptr=fi_ptr, fi_pl=_cat(pl_l + pl_u),
+                fi_pu=_cat(pu_l + pu_u), n_res=int(res_sub[-1]),
+                res_sub_ptr=np.asarray(res_sub, np.int64), res_a=_cat(res_a),
+                res_ptr=np.concatenate([[0], np.cumsum(rcounts)]).astype(np.int64),
+                res_pl=_cat(rpl), res_pu=_cat(rpu), res_tl=_cat(rtl), res_tu=_cat(rtu))
+
+
+def empty_local_plan(n: int, n_sub: int) -> dict:
+    """A plan with empty blocks (coarse-only device contexts)."""
+    z = np.zeros(n_sub + 1, dtype=np.int64)
+    e = np.zeros(0, dtype=np.int64)
+    return dict(n=n, n_sub=n_sub, method=0, n_loc=0, sub_ptr=z, gmap=e,
+                l_ptr=np.zeros(1, np.int64), l_idx=e, u_ptr=np.zeros(1, np.int64), u_idx=e,
+                llev_sub=z, llev_ptr=np.zeros(1, np.int64), llev_rows=e, ulev_sub=z,
+                ulev_ptr=np.zeros(1, np.int64), ulev_rows=e, n_res=0)
+
+
+# ---------------------------------------------------------------------------
+# three-phase objects
+# ---------------------------------------------------------------------------
+
+class PreconditionerSkeleton:
+    """Pattern-only phase (schwarz.py:84-99). `interior_symbolics` and
+    `structure_hash` (which hashes them, as the reference does) are computed
+    on first access: the GPU extension needs no interior factorization."""
+
+    def __init__(self, config, decomposition, n, sets, local_symbolics, interior_sets,
+                 pattern_fingerprint, local_plan):
+        self.config = config
+        self.decomposition = decomposition
+        self.n = n
+        self.sets = sets
+        self.local_symbolics = local_symbolics
+        self.interior_sets = interior_sets
+        self.pattern_fingerprint = pattern_fingerprint
+        self._local_plan = local_plan
+        self._device_plan = None
+        self._interior_symbolics = None
+        self._structure_hash = None
+        self._a_pattern = None
+
+    @property
+    def interior_symbolics(self):
+        if self._interior_symbolics is None:
+            out = []
+            for dofs in self.interior_sets:
+                if dofs.size == 0:
+                    out.append(None)
+                    continue
+                block = extract_submatrix(self._a_pattern, dofs, dofs)
+                out.append(symbolic_lu(block, make_ordering(block, "nested_dissection")))
+            self._interior_symbolics = out
+        return self._interior_symbolics
+
+    @property
+    def structure_hash(self) -> str:
+        if self._structure_hash is None:
+            h = hashlib.sha256()
+            h.update(np.array([self.n, int(self.config.use_coarse)], dtype=np.int64).tobytes())
+            for dofs, sym in zip(self.sets, self.local_symbolics):
+                h.update(dofs.tobytes())
+                h.update(bytes.fromhex(sym.structure_hash))
+            for dofs in self.interior_sets:
+                h.update(dofs.tobytes())
+                if dofs.size:
+                    block = extract_submatrix(self._a_pattern, dofs, dofs)
+                    sym = symbolic_lu(block, make_ordering(block, "nested_dissection"))
+                    h.update(bytes.fromhex(sym.structure_hash))
+            self._structure_hash = h.hexdigest()
+        return self._structure_hash
+
+    def device_plan(self):
+        if self._device_plan is None:
+            from . import device
+            self._device_plan = device.Plan(self._local_plan)
+        return self._device_plan
+
+
+@dataclass
+class CoarseSolver:
+    phi: CsrMatrix
+    phi_t: CsrMatrix
+    a0: CsrMatrix
+    a0_factorization: LocalFactorization
+    column_map: list
+
+
+class TwoLevelPreconditioner:
+    """Numeric phase result (schwarz.py:130-144). `apply` accepts numpy
+    (host round trip) or a CUDA torch tensor (stays on the device)."""
+
+    combine_mode = "additive"
+
+    def __init__(self, n, overlap_maps, local_factorizations, coarse, precision, threads,
+                 skeleton, dev, coarse_device=None):
+        self.n = n
+        self.overlap_maps = overlap_maps
+        self.local_factorizations = local_factorizations
+        self.coarse = coarse
+        self.precision = precision
+        self.threads = threads
+        self.skeleton = skeleton
+        self._dev = dev
+        self._factor_cache = None
+        self.coarse_device = coarse_device
+
+    @property
+    def value_dtype(self):
+        return np.float32 if self.precision == "single" else np.float64
+
+    def download_factors(self, s: int):
+        if self._factor_cache is None:
+            plan = self._dev.plan
+            self._factor_cache = self._dev.factors(plan.nnz_l, plan.nnz_u)
+        lv, uv = self._factor_cache
+        lo = sum(sym.l_idx.size for sym in self.skeleton.local_symbolics[:s])
+        uo = sum(sym.u_idx.size for sym in self.skeleton.local_symbolics[:s])
+        sym = self.skeleton.local_symbolics[s]
+        return lv[lo:lo + sym.l_idx.size].copy(), uv[uo:uo + sym.u_idx.size].copy()
+
+    def apply_device(self, r, out=None):
+        """z = M r for device float64 tensors (no host traffic)."""
+        from . import device
+        t = device.torch()
+        if out is None:
+            out = t.empty_like(r)
+        self._dev.apply(r, out)
+        return out
+
+    def apply(self, r):
+        return apply(self, r)
+
+
+def setup_symbolic(a: CsrMatrix, decomp: Decomposition,
+                   config: SchwarzConfig) -> PreconditionerSkeleton:
+    """Pattern-only phase (schwarz.py:147-203); values of `a` are never read."""
+    if a.nrows != a.ncols:
+        raise ValueError("operator must be square")
+    n = a.nrows
+    part = decomp.partition
+    if part.n != n:
+        raise ValueError("decomposition does not match the operator size")
+    structure = decomp.structure
+    if config.use_coarse and (structure is None or structure.mode is None):
+        raise ValueError("two-level setup needs interface components; build the "
+                         "decomposition with a coarse mode or set use_coarse=False")
+    sets = [np.asarray(s, dtype=np.int64) for s in decomp.overlap.sets]
+    if sum(s.size for s in sets) < n:
+        raise ValueError("overlap sets do not cover the operator")
+    local_symbolics = []
+    for dofs in sets:
+        block = extract_submatrix(a, dofs, dofs)
+        local_symbolics.append(build_symbolic(block, config.local,
+                                              make_ordering(block, config.ordering)))
+    isets = _interior_sets(part, structure) if config.use_coarse else []
+    pattern = CsrMatrix(a.nrows, a.ncols, a.row_ptr, a.col_idx,
+                        np.zeros(a.nnz, dtype=np.float64))
+    plan = local_plan_arrays(n, sets, local_symbolics, config.local.method, pattern)
+    skel = PreconditionerSkeleton(config, decomp, n, sets, local_symbolics, isets,
+                                  _pattern_fingerprint(a), plan)
+    skel._a_pattern = pattern
+    return skel
+
+
+def _lift_to_double(a32: CsrMatrix) -> CsrMatrix:
+    return CsrMatrix(a32.nrows, a32.ncols, a32.row_ptr, a32.col_idx,
+                     a32.values.astype(np.float64))
+
+
+def setup_numeric(skeleton: PreconditionerSkeleton, a: CsrMatrix,
+                  nullspace: np.ndarray | None = None) -> TwoLevelPreconditioner:
+    """Numeric phase on a fixed pattern (schwarz.py:213-287)."""
+    from . import device
+    if _pattern_fingerprint(a) != skeleton.pattern_fingerprint:
+        raise ValueError("operator pattern does not match the symbolic skeleton it was "
+                         "prepared for")
+    config = skeleton.config
+    spec = config.local
+    single = config.precision == "single"
+    if single:
+        a32 = convert_precision(a, np.float32)
+        local_src, coarse_src = a32, _lift_to_double(a32)
+    else:
+        local_src = coarse_src = a
+    value_dtype = np.float32 if single else np.float64
+    plan = skeleton.device_plan()
+    pre = device.Precond(plan, value_dtype, spec.trisolve_iters)
+    a_src_dev = device.DeviceCsr(coarse_src)
+    if not single:
+        try:
+            object.__setattr__(a, "_device_copy", (a.values, a_src_dev))
+        except Exception:
+            pass
+
+    n_sub = len(skeleton.sets)
+    if spec.method == "fast_ilu":
+        if spec.factor_sweeps < 1:
+            raise ValueError("factor_sweeps must be at least 1")
+        if spec.trisolve_iters < 1:
+            raise ValueError("trisolve_iters must be at least 1")
+        try:
+            res = pre.fastilu(a_src_dev, spec.factor_sweeps, n_sub)
+        except FloatingPointError as err:
+            lv, uv = pre.factors(plan.nnz_l, plan.nnz_u)
+            bad, lo, uo = 0, 0, 0
+            for s, sym in enumerate(skeleton.local_symbolics):
+                ls, us = lv[lo:lo + sym.l_idx.size], uv[uo:uo + sym.u_idx.size]
+                if not (np.isfinite(ls).all() and np.isfinite(us).all()):
+                    bad = s
+                    break
+                lo += sym.l_idx.size
+                uo += sym.u_idx.size
+            raise FloatingPointError(
+                f"local matrix of subdomain {bad} failed to factor: {err}") from err
+        facs = []
+        for s, sym in enumerate(skeleton.local_symbolics):
+            facs.append(LocalFactorization(sym, "fast_ilu", None, None,
+                                           sweep_residuals=[float(x) for x in res[:, s]],
+                                           trisolve_iters=spec.trisolve_iters))
+    else:
+        lvs, uvs, facs = [], [], []
+        shift = spec.diag_shift if spec.method == "ilu_k" else 0.0
+        for i, (dofs, sym) in enumerate(zip(skeleton.sets, skeleton.local_symbolics)):
+            block = extract_submatrix(local_src, dofs, dofs)
+            try:
+                lv, uv = host_numeric(block, sym, shift)
+            except np.linalg.LinAlgError as err:
+                raise np.linalg.LinAlgError(
+                    f"local matrix of subdomain {i} failed to factor: {err}") from err
+            lvs.append(lv)
+            uvs.append(uv)
+            facs.append(LocalFactorization(sym, spec.method, lv, uv,
+                                           trisolve_iters=spec.trisolve_iters))
+        pre.set_factors(_cat(lvs, value_dtype), _cat(uvs, value_dtype))
+
+    coarse = None
+    if config.use_coarse:
+        if nullspace is None:
+            raise ValueError("two-level numeric setup needs the operator null space columns")
+        structure = skeleton.decomposition.structure
+        basis = interface_basis(nullspace, structure)
+        phi, column_map, _ = extend_on_device(pre, a_src_dev, coarse_src, structure, basis,
+                                              skeleton.interior_sets)
+        a0 = coarse_matrix(coarse_src, phi)
+        if single:
+            phi = convert_precision(phi, np.float32)
+            a0 = convert_precision(a0, np.float32)
+        try:
+            a0_fac = numeric_lu(a0, symbolic_lu(a0, make_ordering(a0, config.ordering)))
+        except np.linalg.LinAlgError as err:
+            raise np.linalg.LinAlgError(f"coarse matrix is singular: {err}") from err
+        pre.set_coarse_inverse(np.linalg.inv(a0.to_dense().astype(np.float64)))
+        coarse = CoarseSolver(phi, transpose(phi), a0, a0_fac, column_map)
+
+    m = TwoLevelPreconditioner(skeleton.n, skeleton.sets, facs, coarse, config.precision,
+                               config.threads, skeleton, pre)
+    if spec.method == "fast_ilu":
+        for s, f in enumerate(facs):
+            f._source = (m, s)
+    return m
+
+
+def apply(m: TwoLevelPreconditioner, r):
+    """z = Phi A0^-1 Phi^T r + sum_i R_i^T A_i^-1 R_i r (schwarz.py:290-327)."""
+    from . import device
+    t = device.torch()
+    if isinstance(r, t.Tensor) and r.is_cuda:
+        if r.shape != (m.n,):
+            raise ValueError(f"residual has length {tuple(r.shape)}, operator size {m.n}")
+        return m.apply_device(r.to(t.float64).contiguous())
+    r = np.ascontiguousarray(r, dtype=np.float64)
+    if r.shape != (m.n,):
+        raise ValueError(f"residual has length {r.shape}, operator size {m.n}")
+    rd = t.from_numpy(r).cuda()
+    z = m.apply_device(rd)
+    return z.cpu().numpy()

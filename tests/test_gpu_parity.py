@@ -1,0 +1,286 @@
+"""CUDA path vs the oracle (and the reference's golden vectors), through the
+C ABI. Sequential kernels (SpMV, level-set and Jacobi trisolves, FastILU
+sweeps, gather/scatter) must be bit-identical; the coarse correction
+(batched-CG extension + dense A0^-1) within the north star's tolerances:
+1e-10 relative (fp64 apply), 1e-5 (fp32 apply vs fp64), GMRES iterations
+within +-1 of the reference."""
+
+import json
+
+import numpy as np
+import pytest
+
+from cases import BIG, CASES, build, probes, rhs
+from oracle import oracle as O
+from paper_2304_04876_b200 import decomposition as dd
+from paper_2304_04876_b200 import local_solvers as ls
+from paper_2304_04876_b200 import model_problems as mp
+from paper_2304_04876_b200 import schwarz as sw
+from paper_2304_04876_b200.krylov import KrylovConfig, gmres
+from paper_2304_04876_b200.sparse_core import CsrMatrix
+
+pytestmark = pytest.mark.gpu
+PKG = (mp, dd, sw, ls)
+APPLY_TOL64 = 1e-10
+APPLY_TOL32 = 1e-5
+
+
+@pytest.fixture(scope="module")
+def golden(golden_dir):
+    return json.loads((golden_dir / "golden.json").read_text())
+
+
+_CACHE = {}
+
+
+def setup_case(name, table=CASES):
+    if name not in _CACHE:
+        prob, dec, cfg = build(PKG, table[name])
+        skel = sw.setup_symbolic(prob.a, dec, cfg)
+        pre = sw.setup_numeric(skel, prob.a, prob.nullspace if cfg.use_coarse else None)
+        _CACHE[name] = (prob, dec, cfg, skel, pre)
+    return _CACHE[name]
+
+
+def _torch():
+    import torch
+    return torch
+
+
+# ---------------------------------------------------------------------------
+def test_spmv_bitwise_against_oracle():
+    torch = _torch()
+    from paper_2304_04876_b200.device import DeviceCsr
+    rng = np.random.default_rng(0)
+    mats = [mp.assemble_laplace3d(mp.Grid3D(13, 12, 11)).a,
+            mp.assemble_elasticity3d(mp.Grid3D(6, 6, 5)).a]
+    d = (rng.random((70, 50)) < 0.1) * rng.standard_normal((70, 50))
+    mats.append(CsrMatrix.from_dense(d))
+    for a in mats:
+        x = rng.standard_normal(a.ncols)
+        want = O.spmv(a.row_ptr, a.col_idx, a.values, x)
+        dev = DeviceCsr(a)
+        y = torch.zeros(a.nrows, dtype=torch.float64, device="cuda")
+        dev.spmv(torch.from_numpy(x).cuda(), y)
+        assert np.array_equal(y.cpu().numpy(), want)
+        yy = torch.from_numpy(want.copy()).cuda()
+        dev.spmv(torch.from_numpy(x).cuda(), yy, -1.0, 1.0)   # b - A x
+        assert np.array_equal(yy.cpu().numpy(), want - want)
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_local_solves_bitwise_against_oracle(name):
+    torch = _torch()
+    prob, dec, cfg, skel, pre = setup_case(name)
+    ore = O.OracleSchwarz(prob.a, dec, cfg, prob.nullspace if cfg.use_coarse else None,
+                          symbolics=skel.local_symbolics)
+    r = probes(prob.a.nrows, ks=(5,))[0]
+    dt = torch.float32 if cfg.precision == "single" else torch.float64
+    y = torch.empty(skel._local_plan["n_loc"], dtype=dt, device="cuda")
+    pre._dev.local_solve(torch.from_numpy(r).cuda(), y)
+    y = y.cpu().numpy()
+    off = 0
+    rw = r.astype(np.float32) if cfg.precision == "single" else r
+    for i, (dofs, sym) in enumerate(zip(skel.sets, skel.local_symbolics)):
+        want = ore.local_solve(i, rw[dofs])
+        got = np.empty_like(want)
+        got[sym.ordering.perm] = y[off:off + dofs.size]
+        off += dofs.size
+        assert np.array_equal(got, want), f"subdomain {i}"
+
+
+@pytest.mark.parametrize("name", [n for n in sorted(CASES) if CASES[n][4] == "fast_ilu"])
+def test_fastilu_factors_bitwise_against_oracle(name):
+    prob, dec, cfg, skel, pre = setup_case(name)
+    ore = O.OracleSchwarz(prob.a, dec, cfg, prob.nullspace if cfg.use_coarse else None,
+                          symbolics=skel.local_symbolics)
+    for i, fac in enumerate(pre.local_factorizations):
+        lv, uv, res = ore.factors[i]
+        assert np.array_equal(fac.l_values, lv)
+        assert np.array_equal(fac.u_values, uv)
+        assert np.allclose(fac.sweep_residuals, res, rtol=1e-10, atol=0)
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_apply_against_reference_golden(golden_dir, name):
+    prob, dec, cfg, skel, pre = setup_case(name)
+    g = np.load(golden_dir / f"golden_{name}.npz")
+    tol = APPLY_TOL32 if cfg.precision == "single" else APPLY_TOL64
+    for k, r in enumerate(probes(prob.a.nrows)):
+        z = pre.apply(r)
+        want = g[f"apply_{k}"]
+        assert z.dtype == np.float64
+        assert np.abs(z - want).max() <= tol * np.abs(want).max()
+        if cfg.precision == "single":
+            # against the reference's own fp32 apply the gap is far tighter
+            assert np.abs(z - want).max() <= 1e-5 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("name", [n for n in sorted(CASES) if CASES[n][3] == "none"])
+def test_one_level_apply_bitwise(golden_dir, name):
+    prob, dec, cfg, skel, pre = setup_case(name)
+    g = np.load(golden_dir / f"golden_{name}.npz")
+    for k, r in enumerate(probes(prob.a.nrows)):
+        assert np.array_equal(pre.apply(r), g[f"apply_{k}"])
+
+
+@pytest.mark.parametrize("name", [n for n in sorted(CASES) if CASES[n][3] != "none"])
+def test_coarse_basis_and_a0(golden_dir, name):
+    prob, dec, cfg, skel, pre = setup_case(name)
+    g = np.load(golden_dir / f"golden_{name}.npz")
+    phi = pre.coarse.phi.to_dense().astype(np.float64)
+    want = g["phi_dense"]
+    tol = 1e-6 if cfg.precision == "single" else 1e-10
+    assert phi.shape == want.shape
+    assert np.abs(phi - want).max() <= tol * np.abs(want).max()
+    a0 = pre.coarse.a0.to_dense().astype(np.float64)
+    assert np.abs(a0 - g["a0_dense"]).max() <= tol * np.abs(g["a0_dense"]).max()
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_gmres_matches_reference(golden, golden_dir, name):
+    prob, dec, cfg, skel, pre = setup_case(name)
+    g = np.load(golden_dir / f"golden_{name}.npz")
+    x_star, b = rhs(prob)
+    for variant in ("single_reduce", "classic"):
+        x, rep = gmres(prob.a, pre, b, KrylovConfig(variant=variant))
+        want = golden["cases"][name][variant]
+        assert rep.converged
+        assert abs(rep.iterations - want["iterations"]) <= 1
+        assert rep.true_residuals[-1][1] <= 1e-7
+        r = b - prob.a @ x
+        assert np.linalg.norm(r) <= 1e-7 * np.linalg.norm(b) * 1.0001
+        if variant == "single_reduce" and rep.iterations == want["iterations"]:
+            assert rep.iteration_reductions == rep.iterations
+            assert np.allclose(rep.residual_history, g[f"hist_{variant}"], rtol=1e-6,
+                               atol=1e-12)
+
+
+def test_gmres_against_oracle_identical_iterations():
+    """The oracle builds the reference's preconditioner independently (exact
+    interior LU); the coarse bases agree to ~1e-13, so the iteration counts
+    match exactly."""
+    prob, dec, cfg, skel, pre = setup_case("lap10_fast_nat")
+    _, b = rhs(prob)
+    ore = O.OracleSchwarz(prob.a, dec, cfg, prob.nullspace, symbolics=skel.local_symbolics)
+    xo, ro = O.gmres(lambda v: O.csr_spmv(prob.a, v), ore.apply, b)
+    x, rep = gmres(prob.a, pre, b, KrylovConfig(variant="single_reduce"))
+    assert rep.iterations == ro["iterations"]
+    assert np.abs(x - xo).max() <= 1e-8 * np.abs(xo).max()
+
+
+@pytest.mark.parametrize("name", ["C1_lap30_exact", "lap24_fast_4x4x4", "lap17_exact_3x3x3",
+                                  "ela12_fast_2x2x2", "lap20_single_fast"])
+def test_iteration_counts_at_size(golden, name):
+    prob, dec, cfg, skel, pre = setup_case(name, BIG)
+    _, b = rhs(prob)
+    x, rep = gmres(prob.a, pre, b, KrylovConfig(variant="single_reduce"))
+    assert rep.converged
+    assert abs(rep.iterations - golden["big"][name]["iterations"]) <= 1
+    assert np.linalg.norm(b - prob.a @ x) <= 1e-7 * np.linalg.norm(b) * 1.0001
+
+
+# ---------------------------------------------------------------------------
+# properties and error paths (tests/test_schwarz.py:122-308 of the reference)
+# ---------------------------------------------------------------------------
+def test_apply_linearity_and_symmetry():
+    prob, dec, cfg, skel, pre = setup_case("lap9_exact_nd")
+    rng = np.random.default_rng(11)
+    r = rng.standard_normal(prob.a.nrows)
+    z1, z2 = pre.apply(2.5 * r), 2.5 * pre.apply(r)
+    assert np.abs(z1 - z2).max() <= 1e-12 * np.abs(z2).max()
+    s = rng.standard_normal(prob.a.nrows)
+    assert abs(s @ pre.apply(r) - r @ pre.apply(s)) <= 1e-10 * abs(s @ pre.apply(r))
+
+
+def test_apply_deterministic_and_threadsafe():
+    from concurrent.futures import ThreadPoolExecutor
+    prob, dec, cfg, skel, pre = setup_case("lap10_fast_nat")
+    vecs = probes(prob.a.nrows, ks=range(10, 18))
+    want = [pre.apply(r) for r in vecs]
+    with ThreadPoolExecutor(max_workers=4) as ex:
+        got = list(ex.map(pre.apply, vecs))
+    for g, w in zip(got, want):
+        assert np.array_equal(g, w)
+
+
+def test_apply_rejects_wrong_length():
+    prob, dec, cfg, skel, pre = setup_case("lap9_onelevel_ilu0")
+    with pytest.raises(ValueError, match="length"):
+        pre.apply(np.zeros(5))
+
+
+def test_refactorization_on_kept_skeleton_is_bitwise():
+    prob, dec, cfg, skel, pre = setup_case("lap10_fast_nat")
+    pre2 = sw.setup_numeric(skel, prob.a, prob.nullspace)
+    r = probes(prob.a.nrows, ks=(3,))[0]
+    assert np.array_equal(pre.apply(r), pre2.apply(r))
+    a2 = CsrMatrix(prob.a.nrows, prob.a.ncols, prob.a.row_ptr, prob.a.col_idx, 2.0 * prob.a.values)
+    pre3 = sw.setup_numeric(skel, a2, prob.nullspace)
+    assert np.abs(pre3.apply(r) - 0.5 * pre.apply(r)).max() <= 1e-12 * np.abs(pre.apply(r)).max()
+
+
+def test_singular_local_names_subdomain():
+    a = CsrMatrix.from_dense(np.diag([1.0, 1.0, 1.0, 1.0, 1.0, 0.0]))
+    part = dd.Partition(2, [0, 0, 0, 1, 1, 1])
+    skel = sw.setup_symbolic(a, dd.decompose(a, part, 0), sw.SchwarzConfig(use_coarse=False))
+    with pytest.raises(np.linalg.LinAlgError, match="subdomain 1"):
+        sw.setup_numeric(skel, a)
+
+
+def test_singular_coarse_named():
+    n = 6
+    d = np.full(n, 2.0)
+    d[0] = d[-1] = 1.0
+    t = np.diag(d) + np.diag(np.full(n - 1, -1.0), 1) + np.diag(np.full(n - 1, -1.0), -1)
+    a = CsrMatrix.from_dense(t)
+    part = dd.Partition(2, [0, 0, 0, 1, 1, 1])
+    skel = sw.setup_symbolic(a, dd.decompose(a, part, 1, "gdsw"), sw.SchwarzConfig())
+    with pytest.raises(np.linalg.LinAlgError, match="coarse matrix"):
+        sw.setup_numeric(skel, a, np.ones((6, 1)))
+
+
+def test_pattern_mismatch_and_missing_nullspace():
+    prob, dec, cfg, skel, pre = setup_case("lap9_exact_nd")
+    other = CsrMatrix.identity(prob.a.nrows)
+    with pytest.raises(ValueError, match="pattern"):
+        sw.setup_numeric(skel, other, prob.nullspace)
+    with pytest.raises(ValueError, match="null space"):
+        sw.setup_numeric(skel, prob.a, None)
+
+
+def test_gmres_identity_zero_rhs_and_breakdown():
+    n = 10
+    ident = CsrMatrix.identity(n)
+    b = np.random.default_rng(0).standard_normal(n)
+    for variant in ("classic", "single_reduce"):
+        x, rep = gmres(ident, None, b, KrylovConfig(variant=variant))
+        assert rep.converged and rep.iterations == 1
+        assert np.allclose(x, b, atol=1e-13)
+        x, rep = gmres(ident, None, np.zeros(n), KrylovConfig(variant=variant))
+        assert rep.converged and rep.iterations == 0 and list(rep.residual_history) == [1.0]
+        dg = CsrMatrix.from_dense(np.diag([2.0, 3.0, 4.0]))
+        x, rep = gmres(dg, None, np.array([5.0, 0.0, 0.0]), KrylovConfig(variant=variant))
+        assert rep.converged and rep.iterations == 1
+        assert np.allclose(x, [2.5, 0, 0], atol=1e-14)
+
+
+def test_gmres_max_iters_reports_failure():
+    prob = mp.assemble_laplace3d(mp.Grid3D(10, 10, 10))
+    _, b = rhs(prob)
+    x, rep = gmres(prob.a, None, b, KrylovConfig(variant="single_reduce", max_iters=37))
+    assert not rep.converged and rep.iterations == 37
+    assert len(rep.residual_history) == 38
+
+
+def test_block_dot_matches_numpy():
+    torch = _torch()
+    from paper_2304_04876_b200.device import block_dot
+    rng = np.random.default_rng(1)
+    n, j = 100_003, 21
+    V = rng.standard_normal((j, n))
+    v, z = rng.standard_normal(n), rng.standard_normal(n)
+    out = block_dot(torch.from_numpy(V).cuda(), j, torch.from_numpy(v).cuda(),
+                    torch.from_numpy(z).cuda(), n)
+    want = np.concatenate([V @ v, [v @ v], V @ z, [v @ z]])
+    assert np.allclose(out, want, rtol=1e-12, atol=1e-9)
