@@ -152,7 +152,9 @@ def test_gmres_matches_reference(golden, golden_dir, name):
         assert np.linalg.norm(r) <= 1e-7 * np.linalg.norm(b) * 1.0001
         if variant == "single_reduce" and rep.iterations == want["iterations"]:
             assert rep.iteration_reductions == rep.iterations
-            assert np.allclose(rep.residual_history, g[f"hist_{variant}"], rtol=1e-6,
+            # fp32 preconditioners round differently in the coarse sums
+            rtol = 1e-4 if cfg.precision == "single" else 1e-6
+            assert np.allclose(rep.residual_history, g[f"hist_{variant}"], rtol=rtol,
                                atol=1e-12)
 
 
