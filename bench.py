@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""bench.py -- BASELINE.json's metric on B200:
+"GDSW-GMRES solve s & iters to 1e-7, 3D Laplace 2M dof/GPU; apply HBM GB/s".
+
+One step = one complete right-preconditioned single-reduce GMRES(30) solve
+of A x = b to rtol 1e-7 (x0 = 0) on config C2 (BASELINE.json configs[1]):
+3D 7-point Laplace 128^3 = 2,097,152 dof per GPU, 4x4x4 = 64 subdomains
+batched per GPU, overlap 1, rGDSW coarse space, FastILU(0, 3 sweeps) +
+FastSpTRSV(5 iterates) local solves, natural ordering, fp64.
+
+* value / ms_per_step: device time of K solves (CUDA events on the solve
+  stream, barrier + synchronize on both sides, max over ranks), inputs
+  resident in HBM.
+* e2e: the same solve through the public API with the right-hand side in
+  pinned host memory and the solution read back every step.
+* roofline: the dominant kernel's algorithmic bytes / its average launch
+  time (CUDA events recorded by libgdsw on the launching stream during the
+  timed region) against MEASURED_PEAKS.json hbm_gbs.
+* cpu_baseline: the oracle (plain-C restatement of the reference's
+  sequential kernels + numpy GMRES) on a bounded sample of the same solve.
+
+--impl reference: the reference's CPU path (the oracle port, entirely on the
+host, its own exact-LU coarse basis) on the same workload, bounded samples.
+Multi-GPU (torchrun): each rank solves its own 2M-dof C2 system (replicas;
+the sharded single-system solve is the next row of the build).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "GDSW-GMRES solve s & iters to 1e-7, 3D Laplace 2M dof/GPU; apply HBM GB/s"
+# iterations of the reference on C2 (measured by running it)
+REFERENCE_ITERATIONS = {(128, 4, "fast_ilu(0,3,5)", "natural", "double"): 82}
+APPLY_PHASES = ("coarse_restrict", "coarse_solve", "gather", "gather_jacobi_lower",
+                "jacobi_lower", "diag_solve", "jacobi_upper", "levelset", "scatter_prolong")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="native", choices=("native", "reference"))
+    p.add_argument("--n", type=int, default=128, help="grid nodes per axis (per GPU)")
+    p.add_argument("--parts", type=int, default=4, help="subdomain boxes per axis (per GPU)")
+    p.add_argument("--solver", default="fast_ilu(0,3,5)")
+    p.add_argument("--ordering", default="natural")
+    p.add_argument("--precision", default="double")
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--cpu-sample-iters", type=int, default=5)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--profile-region", action="store_true",
+                   help="cudaProfilerStart/Stop around the timed region (ncu --profile-from-start off)")
+    return p.parse_args()
+
+
+def solver_spec(token: str):
+    from paper_2304_04876_b200.local_solvers import SolverSpec
+    name = token.split("(")[0]
+    args = [int(x) for x in token[token.index("(") + 1:-1].split(",")] if "(" in token else []
+    if name == "exact_lu":
+        return SolverSpec("exact_lu")
+    if name == "ilu_k":
+        return SolverSpec("ilu_k", *(args[:1] or [0]))
+    fill, sweeps, iters = (args + [0, 3, 5][len(args):])[:3]
+    return SolverSpec("fast_ilu", fill, sweeps, iters)
+
+
+def build_problem(args):
+    from paper_2304_04876_b200.decomposition import box_partition, decompose
+    from paper_2304_04876_b200.model_problems import Grid3D, assemble_laplace3d
+    from paper_2304_04876_b200.schwarz import SchwarzConfig
+    prob = assemble_laplace3d(Grid3D(args.n, args.n, args.n))
+    part = box_partition(prob.grid, args.parts, args.parts, args.parts)
+    dec = decompose(prob.a, part, 1, "rgdsw")
+    cfg = SchwarzConfig(local=solver_spec(args.solver), ordering=args.ordering,
+                        precision=args.precision)
+    return prob, dec, cfg
+
+
+def workload(args) -> dict:
+    n = args.n ** 3
+    return {"workload": (f"C2: 3D Laplace 7-pt {args.n}^3 ({n:,} dof per GPU), "
+                         f"{args.parts}x{args.parts}x{args.parts}={args.parts ** 3} subdomains "
+                         f"per GPU, overlap 1, rGDSW, {args.solver} local solves, "
+                         f"{args.ordering} ordering, {args.precision} preconditioner, "
+                         "single-reduce GMRES(30) to rtol 1e-7, x0=0"),
+            "dof_per_gpu": n, "subdomains_per_gpu": args.parts ** 3,
+            "parallelism": f"replicas x{args.gpus} (one independent C2 system per GPU)",
+            "l2": "no flush: per-solve working set (A, factors, Phi panels, 2x30 Krylov "
+                  "vectors ~1.9 GB) >> 126 MB L2"}
+
+
+def peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+class Clocks:
+    """nvidia-smi sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.fh = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.fh.seek(0)
+        rows = [r.split(",") for r in self.fh.read().strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for name, v in zip(names, r[5:9]):
+                if v.strip() == "Active":
+                    reasons.add(name)
+        load = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(load), "sm_max_mhz": float(rows[0][2]),
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def native(args):
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2304_04876_b200 import device
+    from paper_2304_04876_b200.krylov import KrylovConfig, gmres
+    from paper_2304_04876_b200.schwarz import setup_numeric, setup_symbolic
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    if world > 1:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            tdist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    t0 = time.perf_counter()
+    prob, dec, cfg = build_problem(args)
+    t_inputs = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    skel = setup_symbolic(prob.a, dec, cfg)
+    t_sym = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    pre = setup_numeric(skel, prob.a, prob.nullspace)
+    torch.cuda.synchronize()
+    t_num = time.perf_counter() - t0
+    n = prob.a.nrows
+    x_star = np.random.default_rng(0).standard_normal(n)
+    b = prob.a @ x_star
+    b_dev = torch.from_numpy(b).cuda()
+    kcfg = KrylovConfig(variant="single_reduce")
+
+    for _ in range(args.warmup):
+        x, rep = gmres(prob.a, pre, b_dev, kcfg)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    device.prof_reset()
+    device.prof_enable(True)
+    l0 = device.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    if args.profile_region:
+        torch.cuda.profiler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    reps = []
+    for _ in range(args.steps):
+        x, rep = gmres(prob.a, pre, b_dev, kcfg)
+        reps.append(rep)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if args.profile_region:
+        torch.cuda.profiler.stop()
+    barrier()
+    clk = clocks.stop()
+    launches = device.launch_count() - l0
+    device.prof_enable(False)
+    phases = device.prof_read()
+    ms_step = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    its = reps[-1].iterations
+    xh = x.cpu().numpy()
+    true_res = float(np.linalg.norm(b - prob.a @ xh) / np.linalg.norm(b))
+    true_err = float(np.linalg.norm(xh - x_star) / np.linalg.norm(x_star))
+
+    peak, peak_kind = peaks()
+    # per-phase achieved bandwidth; dominant = most device time
+    table = {}
+    for name, ph in phases.items():
+        if ph["launches"] == 0 or ph["ms"] <= 0:
+            continue
+        table[name] = dict(ms_total=ph["ms"], launches=ph["launches"],
+                           us_per_launch=1e3 * ph["ms"] / ph["launches"],
+                           bytes_per_launch=ph["bytes"] / ph["launches"],
+                           gbs=ph["bytes"] / (ph["ms"] * 1e-3) / 1e9)
+    dom = max(table, key=lambda k: table[k]["ms_total"])
+    d = table[dom]
+    app_ms = sum(table[k]["ms_total"] for k in APPLY_PHASES if k in table)
+    app_bytes = sum(phases[k]["bytes"] for k in APPLY_PHASES if k in table)
+    n_apply = max(1, phases.get("scatter_prolong", {}).get("launches", 1))
+    apply_gbs = app_bytes / (app_ms * 1e-3) / 1e9 if app_ms else None
+    solve_ms = e0.elapsed_time(e1) / args.steps
+    step_bytes = sum(ph["bytes"] for ph in phases.values()) / args.steps
+    result = {
+        "metric": METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference generators (assemble_laplace3d), x*=default_rng(0)."
+                "standard_normal(n), b=A x*",
+        "config": workload(args),
+        "iterations": its, "converged": bool(reps[-1].converged),
+        "ms_per_iteration": ms_step / max(its, 1),
+        "true_rel_residual": true_res, "true_error": true_err,
+        "apply_gbs": apply_gbs, "apply_frac_of_hbm": apply_gbs / peak if apply_gbs else None,
+        "apply_ms": app_ms / n_apply,
+        "solve_gbs": step_bytes / (solve_ms * 1e-3) / 1e9,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": d["gbs"], "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": d["gbs"] / peak,
+                     "traffic": None, "us_per_launch": d["us_per_launch"],
+                     "bytes_per_launch": d["bytes_per_launch"]},
+        "phases": {k: {kk: round(vv, 4) for kk, vv in v.items()} for k, v in table.items()},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "setup_s": {"inputs": t_inputs, "symbolic_host": t_sym, "numeric": t_num},
+    }
+    if not args.no_e2e:
+        bh = torch.from_numpy(b).pin_memory()
+        for _ in range(1):
+            gmres(prob.a, pre, bh, kcfg)
+        torch.cuda.synchronize()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.e2e_steps):
+            xe, repe = gmres(prob.a, pre, bh, kcfg)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = max_over_ranks(f0.elapsed_time(f1) / args.e2e_steps)
+        result["e2e"] = {"value": e2e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": n * 8,
+                         "d2h_bytes_per_step": n * 8 + 8 * 2 * 31 * repe.iterations,
+                         "api": "paper_2304_04876_b200.krylov.gmres(A, M, pinned host b)"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        result["cpu_baseline"] = cpu_baseline(args, prob, dec, cfg, skel, pre, b, its)
+    if world > 1:
+        tdist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+
+
+def _oracle_sample(ore, prob, b, sample_iters: int):
+    from oracle import oracle as O
+    t0 = time.perf_counter()
+    _, rep = O.gmres(lambda v: O.csr_spmv(prob.a, v), ore.apply, b, max_iters=sample_iters)
+    return (time.perf_counter() - t0) / max(rep["iterations"], 1)
+
+
+def cpu_baseline(args, prob, dec, cfg, skel, pre, b, iterations):
+    """Oracle port, 1 thread, BLAS pinned to 1 thread, on a bounded sample of
+    the same solve (the preconditioner's coarse basis taken from the GPU
+    setup; local factors from the oracle's own FastILU)."""
+    from oracle import oracle as O
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    try:
+        from threadpoolctl import threadpool_limits
+        limiter = threadpool_limits(1)
+    except Exception:
+        limiter = None
+    ore = O.OracleSchwarz(prob.a, dec, cfg, None, symbolics=skel.local_symbolics,
+                          threads=os.cpu_count() or 1,
+                          coarse_parts=(pre.coarse.phi, pre.coarse.a0))
+    per_it = _oracle_sample(ore, prob, b, args.cpu_sample_iters)
+    if limiter is not None:
+        limiter.unregister() if hasattr(limiter, "unregister") else None
+    return {"value": per_it * iterations, "unit": "s", "cores": 1, "kind": "port",
+            "per_iteration_s": per_it,
+            "sample": f"oracle single-reduce GMRES, {args.cpu_sample_iters} iterations of the "
+                      f"C2 solve on 1 core (BLAS 1 thread), per-iteration time x {iterations} "
+                      "iterations; oracle FastILU factors, coarse basis from the GPU setup"}
+
+
+def reference(args):
+    """The reference's CPU implementation of the path (oracle port) on this
+    host: full CPU setup (FastILU, exact-LU harmonic extension), then bounded
+    GMRES samples of the same solve."""
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    cores = os.cpu_count() or 1
+    prob, dec, cfg = build_problem(args)
+    t0 = time.perf_counter()
+    ore = O.OracleSchwarz(prob.a, dec, cfg, prob.nullspace, threads=cores)
+    t_setup = time.perf_counter() - t0
+    x_star = np.random.default_rng(0).standard_normal(prob.a.nrows)
+    b = prob.a @ x_star
+    key = (args.n, args.parts, args.solver, args.ordering, args.precision)
+    iters = REFERENCE_ITERATIONS.get(key)
+    if iters is None:
+        _, rep = O.gmres(lambda v: O.csr_spmv(prob.a, v), ore.apply, b)
+        iters = rep["iterations"]
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
+    for _ in range(args.warmup):
+        _oracle_sample(ore, prob, b, args.cpu_sample_iters)
+    per = [_oracle_sample(ore, prob, b, args.cpu_sample_iters) for _ in range(args.steps)]
+    per_it = float(np.mean(per))
+    value = per_it * iters
+    sample = (f"oracle port of the reference path (plain-C sequential kernels + numpy "
+              f"single-reduce GMRES), each step {args.cpu_sample_iters} GMRES iterations of "
+              f"the C2 solve on 1 core, per-iteration time x {iters} iterations (the "
+              f"reference's count on C2); setup {t_setup:.1f}s on {cores} threads not timed")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * per_it *
+        args.cpu_sample_iters, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference generators, x*=default_rng(0).standard_normal(n), b=A x*",
+        "config": workload(args), "iterations": iters, "ms_per_iteration": 1e3 * per_it,
+        "cpu_baseline": {"value": value, "unit": "s", "cores": 1, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference(args)
+    else:
+        native(args)
+
+
+if __name__ == "__main__":
+    main()

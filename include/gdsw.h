@@ -204,6 +204,7 @@ int gdsw_block_dot(const double* V, int64_t ldv, int32_t j, const double* v, con
  * Instrumentation: per-phase device time (CUDA events on the launching
  * stream) accumulated while enabled. names: see gdsw_prof_name().
  * ---------------------------------------------------------------------- */
+int64_t gdsw_launch_count(void); /* kernels launched by this library so far */
 int gdsw_prof_enable(int on);
 int gdsw_prof_reset(void);
 int gdsw_prof_count(void);

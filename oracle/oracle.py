@@ -223,7 +223,10 @@ class OracleSchwarz:
     """CPU restatement of setup_numeric + apply. `symbolics` are the
     product's host SymbolicFactorizations of the overlap blocks."""
 
-    def __init__(self, a, dec, config, nullspace=None, symbolics=None, threads: int = 1):
+    def __init__(self, a, dec, config, nullspace=None, symbolics=None, threads: int = 1,
+                 coarse_parts=None):
+        """coarse_parts=(phi, a0): take a ready coarse basis (timing samples
+        only) instead of the exact-LU harmonic extension."""
         from paper_2304_04876_b200 import local_solvers as L
         from paper_2304_04876_b200.sparse_core import (CsrMatrix, convert_precision,
                                                        extract_submatrix)
@@ -258,7 +261,9 @@ class OracleSchwarz:
         with ThreadPoolExecutor(max_workers=max(1, threads)) as ex:
             self.factors = list(ex.map(one, range(len(self.sets))))
         self.coarse = None
-        if config.use_coarse:
+        if config.use_coarse and coarse_parts is not None:
+            self.coarse = _coarse_from_parts(*coarse_parts, config)
+        elif config.use_coarse:
             self.coarse = _oracle_coarse(coarse_src, dec, nullspace, config, self.single, threads)
 
     def local_solve(self, i, b):
@@ -284,6 +289,18 @@ class OracleSchwarz:
         if zc is not None:
             z = zc + z
         return z.astype(np.float64) if self.single else z
+
+
+def _coarse_from_parts(phi, a0, config):
+    import scipy.sparse as sp
+    from paper_2304_04876_b200 import local_solvers as L
+    from paper_2304_04876_b200.sparse_core import CsrMatrix
+    a0_sym = L.symbolic_lu(a0, L.make_ordering(a0, config.ordering))
+    a0_l, a0_u = lu_numeric(a0, a0_sym)
+    pt = sp.csr_matrix((phi.values, phi.col_idx, phi.row_ptr), shape=phi.shape).T.tocsr()
+    pt.sort_indices()
+    phi_t = CsrMatrix(phi.ncols, phi.nrows, pt.indptr, pt.indices, pt.data)
+    return phi, phi_t, a0_sym, a0_l, a0_u
 
 
 def _oracle_coarse(a, dec, nullspace, config, single, threads):

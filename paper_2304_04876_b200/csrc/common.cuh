@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -34,7 +35,17 @@ inline void cuda_check(cudaError_t e, const char* what) {
     throw Error(E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 #define CK(x) ::gdsw::cuda_check((x), #x)
-#define CK_LAUNCH() ::gdsw::cuda_check(cudaGetLastError(), "kernel launch")
+// every kernel launch site is followed by CK_LAUNCH(): it checks the launch
+// and counts it (gdsw_launch_count, reported as gpu_launches by bench.py)
+inline std::atomic<int64_t>& launch_counter() {
+  static std::atomic<int64_t> c{0};
+  return c;
+}
+#define CK_LAUNCH()                                                   \
+  do {                                                                \
+    ::gdsw::cuda_check(cudaGetLastError(), "kernel launch");          \
+    ::gdsw::launch_counter().fetch_add(1, std::memory_order_relaxed); \
+  } while (0)
 
 inline void require(bool ok, const std::string& msg, int code = E_VALUE) {
   if (!ok) throw Error(code, msg);

@@ -548,37 +548,46 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   T* X2 = (T*)m->x2.p;
   SellDev L = P->l_sell.view(), U = P->u_sell.view();
   const unsigned g = grid_for(n, TB);
-  const double lbytes = (double)P->nnz_l * (sizeof(T) + 4) + n * (4.0 + 3 * sizeof(T));
-  const double ubytes = (double)P->nnz_u * (sizeof(T) + 4) + n * (4.0 + 3 * sizeof(T));
+  const double lbytes = (double)P->nnz_l * (sizeof(T) + 4) + n * (2.0 + 3 * sizeof(T));
+  const double ubytes = (double)(P->nnz_u - n) * (sizeof(T) + 4) + n * (2.0 + 3 * sizeof(T));
+  // algorithmic bytes per launch: SELL values+columns once, row lengths,
+  // b and x read once (gathers assumed cached), x_new written; the gather
+  // variant reads r through gmap (4 + 8 per row, twice for the neighbours'
+  // rows which are L2-resident) and writes b as well
   T* F;
-  {
-    ProfScope ps("jacobi_lower", s, iters > 1 ? lbytes * (iters - 1) + n * (4.0 + 8.0) : n * (12.0 + sizeof(T)));
-    if (iters <= 1) {
-      k_gather<T><<<g, TB, 0, s>>>(n, P->gmap.p, r, B);
-      CK_LAUNCH();
-      F = B;
-    } else {
+  if (iters <= 1) {
+    ProfScope ps("gather", s, n * (4.0 + 8.0 + sizeof(T)));
+    k_gather<T><<<g, TB, 0, s>>>(n, P->gmap.p, r, B);
+    CK_LAUNCH();
+    F = B;
+  } else {
+    {
+      ProfScope ps("gather_jacobi_lower", s, lbytes + n * (12.0 - sizeof(T)));
       k_gather_jacobi_lower<T><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, P->gmap.p, r, B, X1);
       CK_LAUNCH();
-      T* cur = X1;
-      T* oth = X2;
-      for (int t = 2; t < iters; ++t) {
-        k_jacobi_lower<T><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth);
-        CK_LAUNCH();
-        std::swap(cur, oth);
-      }
-      F = cur;
     }
+    T* cur = X1;
+    T* oth = X2;
+    for (int t = 2; t < iters; ++t) {
+      ProfScope ps("jacobi_lower", s, lbytes);
+      k_jacobi_lower<T><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth);
+      CK_LAUNCH();
+      std::swap(cur, oth);
+    }
+    F = cur;
   }
   T* G = (F == B) ? X1 : B;
   T* H = (F == X2) ? X1 : X2;
   if (F == X1) { G = B; H = X2; }
-  ProfScope ps("jacobi_upper", s, ubytes * (iters - 1) + n * 3.0 * sizeof(T));
-  k_diag_solve<T><<<g, TB, 0, s>>>(n, (const T*)m->udiag.p, F, G);
-  CK_LAUNCH();
+  {
+    ProfScope ps("diag_solve", s, n * 3.0 * sizeof(T));
+    k_diag_solve<T><<<g, TB, 0, s>>>(n, (const T*)m->udiag.p, F, G);
+    CK_LAUNCH();
+  }
   T* cur = G;
   T* oth = H;
   for (int t = 1; t < iters; ++t) {
+    ProfScope ps("jacobi_upper", s, ubytes + n * (double)sizeof(T));
     k_jacobi_upper<T><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, cur, oth);
     CK_LAUNCH();
     std::swap(cur, oth);
@@ -1368,6 +1377,8 @@ int gdsw_block_dot(const double* V, int64_t ldv, int32_t j, const double* v, con
 }
 
 // ---------------------------------------------------------------------------
+int64_t gdsw_launch_count(void) { return launch_counter().load(); }
+
 int gdsw_prof_enable(int on) {
   prof().on = on != 0;
   return GDSW_OK;

@@ -79,6 +79,7 @@ _SIGS = {
                              C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "gdsw_block_dot": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
                                  C.c_int64, C.c_void_p, C.c_void_p]),
+    "gdsw_launch_count": (C.c_int64, []),
     "gdsw_prof_enable": (C.c_int, [C.c_int]),
     "gdsw_prof_reset": (C.c_int, []),
     "gdsw_prof_count": (C.c_int, []),
@@ -369,6 +370,10 @@ def block_dot(V, j: int, v, z, n: int) -> np.ndarray:
 # ---------------------------------------------------------------------------
 # instrumentation
 # ---------------------------------------------------------------------------
+def launch_count() -> int:
+    return int(_lib.gdsw_launch_count())
+
+
 def prof_enable(on: bool = True):
     _ck(_lib.gdsw_prof_enable(1 if on else 0))
 

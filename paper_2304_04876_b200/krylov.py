@@ -128,10 +128,16 @@ def gmres(a, m, b, cfg: KrylovConfig = KrylovConfig(), x0=None):
     from . import device
     t = device.torch()
     on_device = isinstance(b, t.Tensor) and b.is_cuda
+    host_tensor = isinstance(b, t.Tensor) and not b.is_cuda
     t0 = time.perf_counter()
     if on_device:
         bd = b.to(t.float64).contiguous()
         n = bd.shape[0]
+    elif host_tensor:
+        # (pinned) host tensor: async H2D copy, result returned on the host
+        bd = b.to(device="cuda", dtype=t.float64, non_blocking=True)
+        n = bd.shape[0]
+        on_device = True
     else:
         bh = np.ascontiguousarray(b, dtype=np.float64)
         n = bh.shape[0]
@@ -153,5 +159,8 @@ def gmres(a, m, b, cfg: KrylovConfig = KrylovConfig(), x0=None):
     if not on_device:
         bd = t.from_numpy(bh).cuda()
     out = device.gmres_device(a_dev, m_pre, m_csr, bd, xd, nonzero, cfg)
-    x = xd if on_device else xd.cpu().numpy()
+    if host_tensor:
+        x = xd.cpu()
+    else:
+        x = xd if on_device else xd.cpu().numpy()
     return x, _report(out, time.perf_counter() - t0)
