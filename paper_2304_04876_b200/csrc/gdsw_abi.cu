@@ -956,6 +956,7 @@ struct gdsw_workspace {
   int32_t R = 0;
   int nblk = 0;
   DBuf<double> V, Zm, W, MC, ZC, XC, RES, partial, dots, coef;
+  DBuf<unsigned> counter;  // last-block ticket of k_block_dot (self-resetting)
   double* h_dots = nullptr;
   double* h_coef = nullptr;
   size_t n_hdots = 0, n_hcoef = 0;
@@ -1012,9 +1013,8 @@ struct Solver {
         if (nrc < 0) nrc = 0;
         int self_here = (self && ci == nch - 1) ? 1 : 0;
         k_block_dot<<<ws->nblk, KDOT_THREADS, 0, s>>>(n, Vb ? Vb + (int64_t)r0 * n : nullptr, n, nrc,
-                                                      self_here, v, z, ws->partial.p);
-        CK_LAUNCH();
-        k_reduce_partials<<<1, 64, 0, s>>>(ws->nblk, W2, ws->partial.p, ws->dots.p + (int64_t)ci * W2);
+                                                      self_here, v, z, ws->partial.p,
+                                                      ws->dots.p + (int64_t)ci * W2, ws->counter.p);
         CK_LAUNCH();
       }
     }
@@ -1308,6 +1308,9 @@ int gdsw_workspace_create(gdsw_workspace** out, int64_t n, int32_t restart) {
     const int nch = (restart + 1 + KDOT_ROWS - 1) / KDOT_ROWS + 1;
     w->partial.alloc((size_t)w->nblk * W2);
     w->dots.alloc((size_t)nch * W2);
+    w->counter.alloc(1);
+    w->counter.zero();
+    CK(cudaDeviceSynchronize());
     w->coef.alloc(2 * (size_t)restart + 4);
     w->n_hdots = (size_t)nch * W2;
     w->n_hcoef = 2 * (size_t)restart + 4;
@@ -1365,6 +1368,9 @@ int gdsw_block_dot(const double* V, int64_t ldv, int32_t j, const double* v, con
     const int nch = std::max(1, (j + KDOT_ROWS - 1) / KDOT_ROWS);
     ws.partial.alloc((size_t)ws.nblk * W2);
     ws.dots.alloc((size_t)nch * W2);
+    ws.counter.alloc(1);
+    ws.counter.zero();
+    CK(cudaDeviceSynchronize());
     CK(cudaMallocHost(&ws.h_dots, (size_t)nch * W2 * sizeof(double)));
     Solver C{nullptr, nullptr, nullptr, nullptr, S(stream), &ws, n};
     std::vector<double> av, az;
@@ -1380,8 +1386,17 @@ int gdsw_block_dot(const double* V, int64_t ldv, int32_t j, const double* v, con
 int64_t gdsw_launch_count(void) { return launch_counter().load(); }
 
 int gdsw_prof_enable(int on) {
-  prof().on = on != 0;
-  return GDSW_OK;
+  return guarded([&] {
+    Prof& P = prof();
+    std::lock_guard<std::mutex> g(P.mu);
+    // events come from a preallocated pool so recording stays ~1 us/launch
+    while (on && P.pool.size() < 16384) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      P.pool.push_back(e);
+    }
+    P.on = on != 0;
+  });
 }
 int gdsw_prof_reset(void) {
   return guarded([&] {

@@ -22,7 +22,9 @@ __global__ void __launch_bounds__(KDOT_THREADS) k_block_dot(int64_t n, const dou
                                                             int64_t ldv, int nr, int self,
                                                             const double* __restrict__ v,
                                                             const double* __restrict__ z,
-                                                            double* __restrict__ partial) {
+                                                            double* __restrict__ partial,
+                                                            double* __restrict__ out,
+                                                            unsigned* __restrict__ counter) {
   double av[KDOT_ROWS + 1], az[KDOT_ROWS + 1];
 #pragma unroll
   for (int r = 0; r <= KDOT_ROWS; ++r) av[r] = az[r] = 0.0;
@@ -55,11 +57,29 @@ __global__ void __launch_bounds__(KDOT_THREADS) k_block_dot(int64_t n, const dou
     }
   }
   __syncthreads();
-  for (int k = threadIdx.x; k < 2 * (KDOT_ROWS + 1); k += blockDim.x) {
+  constexpr int W2 = 2 * (KDOT_ROWS + 1);
+  for (int k = threadIdx.x; k < W2; k += blockDim.x) {
     double s = 0.0;
     for (int w = 0; w < KDOT_THREADS / 32; ++w) s += red[w][k];
-    partial[(int64_t)blockIdx.x * 2 * (KDOT_ROWS + 1) + k] = s;
+    partial[(int64_t)blockIdx.x * W2 + k] = s;
   }
+  // last block to finish reduces all block partials in a fixed order (one
+  // warp per value, lanes strided over blocks, fixed shuffle tree): the
+  // second stage costs no extra launch and stays deterministic
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int k = warp; k < W2; k += KDOT_THREADS / 32) {
+    double s = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(partial + (int64_t)b * W2 + k);
+    s = warp_sum(s);
+    if (lane == 0) out[k] = s;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
 }
 
 // out[k] = sum over blocks (ascending) of partial[blk][k]
