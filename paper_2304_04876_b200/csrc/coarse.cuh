@@ -68,6 +68,128 @@ __global__ void k_restrict_final(RestrictDev R, const T* __restrict__ pgt_val,
   }
 }
 
+// ---------------------------------------------------------------------------
+// chunked restriction / prolongation (chunks of <= 256 interior rows that
+// never straddle a subdomain, shared with the extension solver)
+// ---------------------------------------------------------------------------
+struct ChunkDev {
+  const int32_t* chunk_sub;
+  const int32_t* chunk_row0;
+  const int32_t* chunk_nrow;
+  const int64_t* chunk_poff;  // partial offset of the chunk's first column
+  const int32_t* int_ptr;
+  const int32_t* int_rows;
+  const int32_t* n_int;
+  const int32_t* col_ptr;
+  const int32_t* col_ids;
+  const int64_t* panel_off;
+};
+
+constexpr int CH_THREADS = 256;
+constexpr int CH_MAXK = 128;
+
+// partial[chunk_poff + c] = sum over the chunk's rows of P[c][row] r[row]
+// (r is read once per row, each panel column streamed coalesced)
+template <typename T>
+__global__ void __launch_bounds__(CH_THREADS) k_restrict_chunks(ChunkDev D, const T* __restrict__ panel,
+                                                                const double* __restrict__ r,
+                                                                T* __restrict__ partial) {
+  __shared__ T red[CH_THREADS / 32][CH_MAXK];
+  const int32_t ch = blockIdx.x;
+  const int32_t s = D.chunk_sub[ch];
+  const int32_t ni = D.n_int[s];
+  const int k = D.col_ptr[s + 1] - D.col_ptr[s];
+  const bool on = threadIdx.x < D.chunk_nrow[ch];
+  const int32_t row = D.chunk_row0[ch] + threadIdx.x;
+  const T rv = on ? (T)r[D.int_rows[D.int_ptr[s] + row]] : T(0);
+  const T* pc = panel + D.panel_off[s] + row;
+  for (int c = 0; c < k; ++c) {
+    T v = on ? ldg_stream(pc + (int64_t)c * ni) * rv : T(0);
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][c] = v;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < k; c += blockDim.x) {
+    T acc = T(0);
+#pragma unroll
+    for (int w = 0; w < CH_THREADS / 32; ++w) acc += red[w][c];
+    partial[D.chunk_poff[ch] + c] = acc;
+  }
+}
+
+// one CTA per coarse column: u[c] = Phi_Gamma^T[c,:] r + sum of its panel
+// partials (flattened list), both as fixed-shape block reductions
+template <typename T>
+__global__ void __launch_bounds__(256) k_restrict_columns(int32_t n_c, const int64_t* __restrict__ pgt_ptr,
+                                                          const int32_t* __restrict__ pgt_row,
+                                                          const T* __restrict__ pgt_val,
+                                                          const double* __restrict__ r,
+                                                          const int64_t* __restrict__ cpart_ptr,
+                                                          const int64_t* __restrict__ cpart_idx,
+                                                          const T* __restrict__ partial,
+                                                          T* __restrict__ u) {
+  const int32_t c = blockIdx.x;
+  T acc = T(0);
+  for (int64_t p = pgt_ptr[c] + threadIdx.x; p < pgt_ptr[c + 1]; p += blockDim.x)
+    acc += pgt_val[p] * (T)r[pgt_row[p]];
+  for (int64_t p = cpart_ptr[c] + threadIdx.x; p < cpart_ptr[c + 1]; p += blockDim.x)
+    acc += partial[cpart_idx[p]];
+  __shared__ T red[8];
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    T t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : T(0);
+    t = warp_sum(t);
+    if (threadIdx.x == 0) u[c] = t;
+  }
+}
+
+// interior rows: z[g] = double( (Phi v)[g] + (0 + y_a + ...) ), Phi row =
+// dense panel row over the subdomain's sorted coarse columns (coalesced)
+template <typename T>
+__global__ void __launch_bounds__(CH_THREADS) k_prolong_interior(ChunkDev D, const T* __restrict__ panel,
+                                                                 const T* __restrict__ v,
+                                                                 const int32_t* __restrict__ sc_ptr,
+                                                                 const int32_t* __restrict__ sc_pos,
+                                                                 const T* __restrict__ y,
+                                                                 double* __restrict__ z) {
+  const int32_t ch = blockIdx.x;
+  if (threadIdx.x >= D.chunk_nrow[ch]) return;
+  const int32_t s = D.chunk_sub[ch];
+  const int32_t ni = D.n_int[s];
+  const int32_t row = D.chunk_row0[ch] + threadIdx.x;
+  const int32_t g = D.int_rows[D.int_ptr[s] + row];
+  const T* pr = panel + D.panel_off[s] + row;
+  T zc = T(0);
+  for (int32_t c = D.col_ptr[s]; c < D.col_ptr[s + 1]; ++c, pr += ni)
+    zc = rn_add(zc, rn_mul(ldg_stream(pr), v[D.col_ids[c]]));
+  T acc = T(0);
+  for (int32_t q = sc_ptr[g]; q < sc_ptr[g + 1]; ++q) acc = rn_add(acc, y[sc_pos[q]]);
+  z[g] = (double)rn_add(zc, acc);
+}
+
+// interface rows: Phi_Gamma row (CSR by interface position) + scatter
+template <typename T>
+__global__ void __launch_bounds__(256) k_prolong_interface(int32_t n_gamma, const int32_t* __restrict__ gamma_rows,
+                                                           const int64_t* __restrict__ pg_ptr,
+                                                           const int32_t* __restrict__ pg_col,
+                                                           const T* __restrict__ pg_val,
+                                                           const T* __restrict__ v,
+                                                           const int32_t* __restrict__ sc_ptr,
+                                                           const int32_t* __restrict__ sc_pos,
+                                                           const T* __restrict__ y,
+                                                           double* __restrict__ z) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n_gamma) return;
+  const int32_t g = gamma_rows[t];
+  T zc = T(0);
+  for (int64_t p = pg_ptr[t]; p < pg_ptr[t + 1]; ++p) zc = rn_add(zc, rn_mul(pg_val[p], v[pg_col[p]]));
+  T acc = T(0);
+  for (int32_t q = sc_ptr[g]; q < sc_ptr[g + 1]; ++q) acc = rn_add(acc, y[sc_pos[q]]);
+  z[g] = (double)rn_add(zc, acc);
+}
+
 // dense replicated coarse solve: v = A0^-1 u, one warp per row
 template <typename T>
 __global__ void k_coarse_gemv(int32_t n_c, const T* __restrict__ ainv, const T* __restrict__ u,

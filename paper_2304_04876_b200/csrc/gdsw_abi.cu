@@ -225,6 +225,14 @@ struct CoarsePlan {
     p.col_ids = col_ids.p;
     return p;
   }
+  // chunked restriction/prolongation tables
+  DBuf<int64_t> cpart_ptr, cpart_idx;
+  int64_t n_cpart = 0;
+  DBuf<int32_t> gamma32;
+  ChunkDev chunk_dev() const {
+    return ChunkDev{chunk_sub.p, chunk_row0.p, chunk_nrow.p, chunk_poff.p, int_ptr.p,
+                    int_rows.p,  n_int.p,      col_ptr.p,    col_ids.p,    panel_off.p};
+  }
   RestrictDev restrict_dev() const {
     return RestrictDev{n_c,       colsub.p,   col_ptr.p,    panel_off.p, n_int.p,
                        int_ptr.p, int_rows.p, pgt_ptr.p,    pgt_row.p,   clist_ptr.p,
@@ -447,6 +455,23 @@ void build_coarse(CoarsePlan* P, const gdsw_plan* L, const gdsw_coarse_desc* c) 
     P->chunk_nrow.upload(cnrow);
     P->chunk_poff.upload(cpoff);
     P->sub_chunk0.upload(sc0);
+    // coarse column -> the chunk partials of every panel column mapping to it
+    // (ascending subdomain, then ascending chunk)
+    std::vector<std::vector<int64_t>> parts(c->n_c);
+    for (int32_t s = 0; s < ns; ++s)
+      for (int64_t k = cptr[s]; k < cptr[s + 1]; ++k)
+        for (int32_t ch = sc0[s]; ch < sc0[s + 1]; ++ch)
+          parts[cids[k]].push_back(cpoff[ch] + (k - cptr[s]));
+    std::vector<int64_t> pp(c->n_c + 1, 0), pidx;
+    for (int32_t k = 0; k < c->n_c; ++k) {
+      pidx.insert(pidx.end(), parts[k].begin(), parts[k].end());
+      pp[k + 1] = (int64_t)pidx.size();
+    }
+    P->n_cpart = (int64_t)pidx.size();
+    P->cpart_ptr.upload(pp);
+    if (pidx.empty()) pidx.push_back(0);
+    P->cpart_idx.upload(pidx);
+    P->gamma32.upload(to_i32(grows.data(), grows.size()));
   }
   {
     std::vector<int64_t> aptr = vec(c->aii_ptr, P->n_int_total + 1);
@@ -620,16 +645,19 @@ void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
   gdsw_plan* P = m->plan;
   CoarsePlan* Cp = m->cp.get();
   if (Cp) {
-    RestrictDev R = Cp->restrict_dev();
+    ChunkDev D = Cp->chunk_dev();
+    if (Cp->n_chunks > 0) {
+      // panels once + r at interior rows (4 B index + 8 B value)
+      ProfScope ps("restrict_panels", s, (double)Cp->panel_entries * sizeof(T) + Cp->n_int_total * 12.0);
+      k_restrict_chunks<T><<<Cp->n_chunks, CH_THREADS, 0, s>>>(D, (const T*)m->panel(), r, (T*)m->pdot.p);
+      CK_LAUNCH();
+    }
     {
-      ProfScope ps("coarse_restrict", s, (double)Cp->panel_entries * sizeof(T) + Cp->n_int_total * 12.0 +
-                                             (double)Cp->h_pgt_val.size() * (sizeof(T) + 12));
-      if (Cp->K > 0) {
-        k_restrict_panels<T><<<Cp->K, TB, 0, s>>>(R, (const T*)m->panel(), r, (T*)m->pdot.p);
-        CK_LAUNCH();
-      }
-      k_restrict_final<T><<<grid_for(Cp->n_c, TB / 32), TB, 0, s>>>(R, (const T*)m->pgt_val.p, r,
-                                                                   (const T*)m->pdot.p, (T*)m->cu.p);
+      ProfScope ps("restrict_columns", s, (double)Cp->h_pgt_val.size() * (sizeof(T) + 12) +
+                                              (double)Cp->n_cpart * (sizeof(T) + 8));
+      k_restrict_columns<T><<<Cp->n_c, 256, 0, s>>>(Cp->n_c, Cp->pgt_ptr.p, Cp->pgt_row.p,
+                                                    (const T*)m->pgt_val.p, r, Cp->cpart_ptr.p,
+                                                    Cp->cpart_idx.p, (const T*)m->pdot.p, (T*)m->cu.p);
       CK_LAUNCH();
     }
     ProfScope ps("coarse_solve", s, (double)Cp->n_c * Cp->n_c * sizeof(T));
@@ -638,14 +666,33 @@ void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
     CK_LAUNCH();
   }
   T* y = local_solve<T>(m, r, 0, s);
-  ProfScope ps("scatter_prolong", s, P->n_loc * (4.0 + sizeof(T)) + (P->n + 1) * 4.0 + P->n * 8.0 +
-                                         (Cp ? (double)Cp->panel_entries * sizeof(T) : 0.0));
-  ProlongDev pro{};
-  if (Cp) pro = Cp->prolong();
-  k_scatter_prolong<T><<<grid_for(P->n, TB), TB, 0, s>>>(
-      (int32_t)P->n, P->sc_ptr.p, P->sc_pos.p, y, pro, (const T*)m->pgr_val.p,
-      (const T*)m->panel(), (const T*)m->cv.p, z);
-  CK_LAUNCH();
+  if (Cp) {
+    ChunkDev D = Cp->chunk_dev();
+    // interior rows: panel row dot (coalesced) + their local contributions
+    if (Cp->n_chunks > 0) {
+      ProfScope ps("prolong_interior", s, (double)Cp->panel_entries * sizeof(T) +
+                                              Cp->n_int_total * (4.0 + 8.0 + 8.0 + 4.0 + sizeof(T)));
+      k_prolong_interior<T><<<Cp->n_chunks, CH_THREADS, 0, s>>>(D, (const T*)m->panel(), (const T*)m->cv.p,
+                                                               P->sc_ptr.p, P->sc_pos.p, y, z);
+      CK_LAUNCH();
+    }
+    const double ng = (double)Cp->n_gamma;
+    ProfScope ps("prolong_interface", s, (double)Cp->h_pgr_val.size() * (sizeof(T) + 4) +
+                                             ng * (4.0 + 8.0 + 8.0 + 8.0) +
+                                             (double)(P->n_loc - Cp->n_int_total) * (4.0 + sizeof(T)));
+    if (Cp->n_gamma > 0) {
+      k_prolong_interface<T><<<grid_for(Cp->n_gamma, TB), TB, 0, s>>>(
+          (int32_t)Cp->n_gamma, Cp->gamma32.p, Cp->pgam_ptr.p, Cp->pgam_col.p, (const T*)m->pgr_val.p,
+          (const T*)m->cv.p, P->sc_ptr.p, P->sc_pos.p, y, z);
+      CK_LAUNCH();
+    }
+  } else {
+    ProfScope ps("scatter", s, P->n_loc * (4.0 + sizeof(T)) + (P->n + 1) * 4.0 + P->n * 8.0);
+    k_scatter_prolong<T><<<grid_for(P->n, TB), TB, 0, s>>>(
+        (int32_t)P->n, P->sc_ptr.p, P->sc_pos.p, y, ProlongDev{}, (const T*)nullptr, (const T*)nullptr,
+        (const T*)nullptr, z);
+    CK_LAUNCH();
+  }
 }
 
 void precond_apply(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
@@ -700,7 +747,7 @@ int gdsw_precond_set_coarse(gdsw_precond* m, const gdsw_coarse_desc* desc) {
       upload_cast<T>(m->pgr_val, cp->h_pgr_val);
       upload_cast<T>(m->pgt_val, cp->h_pgt_val);
     });
-    m->pdot.alloc(std::max<int32_t>(cp->K, 1) * m->es);
+    m->pdot.alloc(std::max<int64_t>(cp->n_partial, 1) * m->es);
     m->cu.alloc(std::max<int32_t>(cp->n_c, 1) * m->es);
     m->cv.alloc(std::max<int32_t>(cp->n_c, 1) * m->es);
     m->panel64.alloc(std::max<int64_t>(cp->panel_entries, 1));
@@ -948,441 +995,10 @@ int gdsw_precond_destroy(gdsw_precond* m) {
 
 }  // extern "C"
 
-// ===========================================================================
-// GMRES (krylov.py)
-// ===========================================================================
-struct gdsw_workspace {
-  int64_t n = 0;
-  int32_t R = 0;
-  int nblk = 0;
-  DBuf<double> V, Zm, W, MC, ZC, XC, RES, partial, dots, coef;
-  DBuf<unsigned> counter;  // last-block ticket of k_block_dot (self-resetting)
-  double* h_dots = nullptr;
-  double* h_coef = nullptr;
-  size_t n_hdots = 0, n_hcoef = 0;
-  ~gdsw_workspace() {
-    if (h_dots) cudaFreeHost(h_dots);
-    if (h_coef) cudaFreeHost(h_coef);
-  }
-};
-
-namespace {
-
-constexpr double BREAKDOWN_REL = 1e-14;  // krylov.py:42
-
-struct Solver {
-  const gdsw_csr* a;
-  gdsw_precond* m;
-  const gdsw_csr* mcsr;
-  const double* b;
-  cudaStream_t s;
-  gdsw_workspace* ws;
-  int64_t n;
-  int iter_red = 0, res_red = 0;
-
-  unsigned vgrid() const { return grid_for(n, TB, (int64_t)num_sms() * 8); }
-
-  void A(const double* x, double* y) {
-    ProfScope ps("spmv", s, (double)a->nnz * 12.0 + (a->nrows + 1) * 4.0 + 2.0 * n * 8.0);
-    spmv_T<double>(a, x, nullptr, y, 0, 1.0, 0.0, s);
-  }
-  void resid(const double* x, double* r) {
-    ProfScope ps("spmv", s, (double)a->nnz * 12.0 + (a->nrows + 1) * 4.0 + 3.0 * n * 8.0);
-    spmv_T<double>(a, x, b, r, 1, -1.0, 1.0, s);
-  }
-  void M(const double* x, double* y) {
-    if (m) {
-      precond_apply(m, x, y, s);
-    } else if (mcsr) {
-      ProfScope ps("spmv", s, (double)mcsr->nnz * 12.0 + 2.0 * n * 8.0);
-      spmv_T<double>(mcsr, x, nullptr, y, 0, 1.0, 0.0, s);
-    } else {
-      CK(cudaMemcpyAsync(y, x, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    }
-  }
-  // rows V[0..nr) (+ v itself when self) against v (and z): host av/az of length nr+1
-  void block(const double* Vb, int nr, bool self, const double* v, const double* z,
-             std::vector<double>& av, std::vector<double>& az) {
-    const int W2 = 2 * (KDOT_ROWS + 1);
-    int nch = std::max(1, (nr + KDOT_ROWS - 1) / KDOT_ROWS);
-    {
-      ProfScope ps("block_dot", s, (double)(nr + (self ? 1 : 0) + (z ? 1 : 0)) * n * 8.0);
-      for (int ci = 0; ci < nch; ++ci) {
-        int r0 = ci * KDOT_ROWS;
-        int nrc = std::min(KDOT_ROWS, nr - r0);
-        if (nrc < 0) nrc = 0;
-        int self_here = (self && ci == nch - 1) ? 1 : 0;
-        k_block_dot<<<ws->nblk, KDOT_THREADS, 0, s>>>(n, Vb ? Vb + (int64_t)r0 * n : nullptr, n, nrc,
-                                                      self_here, v, z, ws->partial.p,
-                                                      ws->dots.p + (int64_t)ci * W2, ws->counter.p);
-        CK_LAUNCH();
-      }
-    }
-    CK(cudaMemcpyAsync(ws->h_dots, ws->dots.p, (size_t)nch * W2 * sizeof(double), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    av.assign(nr + 1, 0.0);
-    az.assign(nr + 1, 0.0);
-    for (int r = 0; r < nr; ++r) {
-      int ci = r / KDOT_ROWS, rr = r % KDOT_ROWS;
-      av[r] = ws->h_dots[ci * W2 + 2 * rr];
-      az[r] = ws->h_dots[ci * W2 + 2 * rr + 1];
-    }
-    if (self) {
-      av[nr] = ws->h_dots[(nch - 1) * W2 + 2 * KDOT_ROWS];
-      az[nr] = ws->h_dots[(nch - 1) * W2 + 2 * KDOT_ROWS + 1];
-    }
-  }
-  double norm(const double* v) {
-    std::vector<double> av, az;
-    block(nullptr, 0, true, v, nullptr, av, az);
-    return std::sqrt(av[0]);
-  }
-  void put_coef(const std::vector<double>& c) {
-    std::copy(c.begin(), c.end(), ws->h_coef);
-    CK(cudaMemcpyAsync(ws->coef.p, ws->h_coef, c.size() * sizeof(double), cudaMemcpyHostToDevice, s));
-  }
-  void xupdate(const double* x, int mcols, const std::vector<double>& y, double* xo) {
-    put_coef(y);
-    ProfScope ps("x_update", s, (double)(mcols + 2) * n * 8.0);
-    k_x_update<<<vgrid(), TB, 0, s>>>(n, x, ws->Zm.p, n, mcols, ws->coef.p, xo);
-    CK_LAUNCH();
-  }
-};
-
-double rotation_hypot(double a, double b) { return std::hypot(a, b); }
-
-// krylov.py:118-130
-double process_column(std::vector<double>& h, int R, std::vector<double>& cs, std::vector<double>& sn,
-                      std::vector<double>& g, int j) {
-  auto H = [&](int i, int k) -> double& { return h[(size_t)i * R + k]; };
-  for (int i = 0; i < j; ++i) {
-    double t = cs[i] * H(i, j) + sn[i] * H(i + 1, j);
-    H(i + 1, j) = -sn[i] * H(i, j) + cs[i] * H(i + 1, j);
-    H(i, j) = t;
-  }
-  double r = rotation_hypot(H(j, j), H(j + 1, j));
-  if (r == 0.0) {
-    cs[j] = 1.0;
-    sn[j] = 0.0;
-  } else {
-    cs[j] = H(j, j) / r;
-    sn[j] = H(j + 1, j) / r;
-  }
-  H(j, j) = cs[j] * H(j, j) + sn[j] * H(j + 1, j);
-  H(j + 1, j) = 0.0;
-  g[j + 1] = -sn[j] * g[j];
-  g[j] = cs[j] * g[j];
-  return std::fabs(g[j + 1]);
-}
-
-// krylov.py:133-138
-std::vector<double> solve_y(const std::vector<double>& h, int R, const std::vector<double>& g, int m) {
-  std::vector<double> y(m, 0.0);
-  for (int i = m - 1; i >= 0; --i) {
-    double dot = 0.0;
-    for (int k = i + 1; k < m; ++k) dot += h[(size_t)i * R + k] * y[k];
-    y[i] = (g[i] - dot) / h[(size_t)i * R + i];
-  }
-  return y;
-}
-
-struct Outcome {
-  int it = 0;
-  bool converged = false;
-  int restarts = 0;
-  std::vector<double> history{1.0};
-  std::vector<std::pair<int, double>> true_res;
-};
-
-void copy_vec(double* dst, const double* src, int64_t n, cudaStream_t s) {
-  if (dst != src) CK(cudaMemcpyAsync(dst, src, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-}
-
-void gmres_single_reduce(Solver& C, double* x, bool x0nz, const gdsw_krylov_cfg& cfg, Outcome& o) {
-  const int R = cfg.restart;
-  const int64_t n = C.n;
-  double* V = C.ws->V.p;
-  double* Zm = C.ws->Zm.p;
-  double* W = C.ws->W.p;
-  double* MC = C.ws->MC.p;
-  double* ZC = C.ws->ZC.p;
-  double* XC = C.ws->XC.p;
-  std::vector<double> h((size_t)(R + 1) * R, 0.0), g(R + 1, 0.0), cs(R, 0.0), sn(R, 0.0);
-  std::vector<double> av, az;
-  bool have_denom = false;
-  double denom = 0.0, bnorm = 0.0;
-  auto H = [&](int i, int k) -> double& { return h[(size_t)i * R + k]; };
-  while (true) {
-    C.resid(x, W);
-    o.restarts++;
-    C.M(W, MC);
-    C.A(MC, ZC);
-    std::fill(g.begin(), g.end(), 0.0);
-    for (int j = 0; j <= R; ++j) {
-      const bool last = j == R;
-      C.block(V, j, true, W, last ? nullptr : ZC, av, az);
-      const double b2 = av[j], q = az[j];
-      if (j == 0) C.res_red++; else C.iter_red++;
-      double aa = 0.0;
-      for (int r = 0; r < j; ++r) aa += av[r] * av[r];
-      const double delta2 = b2 - aa;
-      const double delta = delta2 > 0.0 ? std::sqrt(delta2) : 0.0;
-      if (j == 0) {
-        if (!have_denom) {
-          have_denom = true;
-          denom = delta;
-          if (x0nz) {
-            C.res_red++;
-            bnorm = [&] {
-              std::vector<double> bv, bz;
-              C.block(nullptr, 0, true, C.b, nullptr, bv, bz);
-              return std::sqrt(bv[0]);
-            }();
-          } else {
-            bnorm = delta;
-          }
-          if (delta <= BREAKDOWN_REL * bnorm) { o.it = 0; o.converged = true; return; }
-        } else {
-          o.true_res.emplace_back(o.it, delta / denom);
-        }
-        if (delta / denom <= cfg.rel_tol) { o.converged = true; return; }
-        g[0] = delta;
-      } else {
-        for (int r = 0; r < j; ++r) H(r, j - 1) += av[r];
-        H(j, j - 1) = delta;
-        o.it++;
-        double est = process_column(h, R, cs, sn, g, j - 1);
-        o.history.push_back(est / denom);
-        const bool breakdown = delta <= BREAKDOWN_REL * bnorm;
-        if (breakdown || est / denom <= cfg.rel_tol || o.it >= cfg.max_iters) {
-          std::vector<double> y = solve_y(h, R, g, j);
-          C.xupdate(x, j, y, XC);
-          C.resid(XC, C.ws->RES.p);
-          C.res_red++;
-          double tr = C.norm(C.ws->RES.p);
-          o.true_res.emplace_back(o.it, tr / denom);
-          if (tr / denom <= cfg.rel_tol) { copy_vec(x, XC, n, C.s); o.converged = true; return; }
-          if (breakdown || o.it >= cfg.max_iters) { copy_vec(x, XC, n, C.s); o.converged = false; return; }
-        }
-      }
-      if (last) break;
-      std::vector<double> coef(2 * j);
-      double ap = 0.0;
-      for (int r = 0; r < j; ++r) ap += av[r] * az[r];
-      const double corr = (q - ap) / (delta * delta);
-      for (int r = 0; r < j; ++r) {
-        coef[r] = av[r];
-        coef[j + r] = az[r] / delta;
-        H(r, j) = az[r] / delta;
-      }
-      H(j, j) = corr;
-      C.put_coef(coef);
-      {
-        ProfScope ps("sr_update", C.s, (double)(2 * j + 6) * n * 8.0);
-        k_sr_update<<<C.vgrid(), TB, 0, C.s>>>(n, V, Zm, n, j, C.ws->coef.p, delta, corr, W, MC, ZC);
-        CK_LAUNCH();
-      }
-      if (j + 1 <= R - 1) {
-        C.M(W, MC);
-        C.A(MC, ZC);
-      }
-    }
-    std::vector<double> y = solve_y(h, R, g, R);
-    C.xupdate(x, R, y, x);
-  }
-}
-
-void gmres_classic(Solver& C, double* x, bool x0nz, const gdsw_krylov_cfg& cfg, Outcome& o) {
-  const int R = cfg.restart;
-  const int64_t n = C.n;
-  double* V = C.ws->V.p;
-  double* Zm = C.ws->Zm.p;
-  double* W = C.ws->W.p;
-  double* XC = C.ws->XC.p;
-  double* RES = C.ws->RES.p;
-  std::vector<double> h((size_t)(R + 1) * R, 0.0), g(R + 1, 0.0), cs(R, 0.0), sn(R, 0.0);
-  std::vector<double> av, az;
-  bool have_denom = false;
-  double denom = 0.0, bnorm = 0.0;
-  auto H = [&](int i, int k) -> double& { return h[(size_t)i * R + k]; };
-  while (true) {
-    C.resid(x, RES);
-    const double beta = C.norm(RES);
-    C.res_red++;
-    o.restarts++;
-    if (!have_denom) {
-      have_denom = true;
-      denom = beta;
-      if (x0nz) {
-        C.res_red++;
-        bnorm = C.norm(C.b);
-      } else {
-        bnorm = beta;
-      }
-      if (beta <= BREAKDOWN_REL * bnorm) { o.it = 0; o.converged = true; return; }
-    } else {
-      o.true_res.emplace_back(o.it, beta / denom);
-    }
-    if (beta / denom <= cfg.rel_tol) { o.converged = true; return; }
-    k_scale_copy<<<C.vgrid(), TB, 0, C.s>>>(n, RES, beta, V);
-    CK_LAUNCH();
-    std::fill(g.begin(), g.end(), 0.0);
-    g[0] = beta;
-    for (int j = 0; j < R; ++j) {
-      double* vj = V + (int64_t)j * n;
-      double* zj = Zm + (int64_t)j * n;
-      C.M(vj, zj);
-      C.A(zj, W);
-      if (cfg.orthogonalization == GDSW_MGS) {
-        for (int i = 0; i <= j; ++i) {
-          C.block(V + (int64_t)i * n, 1, false, W, nullptr, av, az);
-          C.iter_red++;
-          const double hij = av[0];
-          k_axpy_scalar<<<C.vgrid(), TB, 0, C.s>>>(n, hij, V + (int64_t)i * n, W);
-          CK_LAUNCH();
-          H(i, j) = hij;
-        }
-      } else {
-        std::vector<double> c1, c2, t;
-        C.block(V, j + 1, false, W, nullptr, c1, t);
-        C.iter_red++;
-        c1.resize(j + 1);
-        C.put_coef(c1);
-        k_multi_axpy<<<C.vgrid(), TB, 0, C.s>>>(n, V, n, j + 1, C.ws->coef.p, W);
-        CK_LAUNCH();
-        C.block(V, j + 1, false, W, nullptr, c2, t);
-        C.iter_red++;
-        c2.resize(j + 1);
-        C.put_coef(c2);
-        k_multi_axpy<<<C.vgrid(), TB, 0, C.s>>>(n, V, n, j + 1, C.ws->coef.p, W);
-        CK_LAUNCH();
-        for (int i = 0; i <= j; ++i) H(i, j) = c1[i] + c2[i];
-      }
-      const double nrm = C.norm(W);
-      C.iter_red++;
-      H(j + 1, j) = nrm;
-      o.it++;
-      double est = process_column(h, R, cs, sn, g, j);
-      o.history.push_back(est / denom);
-      const bool breakdown = nrm <= BREAKDOWN_REL * bnorm;
-      if (breakdown || est / denom <= cfg.rel_tol || o.it >= cfg.max_iters) {
-        std::vector<double> y = solve_y(h, R, g, j + 1);
-        C.xupdate(x, j + 1, y, XC);
-        C.resid(XC, RES);
-        C.res_red++;
-        double tr = C.norm(RES);
-        o.true_res.emplace_back(o.it, tr / denom);
-        if (tr / denom <= cfg.rel_tol) { copy_vec(x, XC, n, C.s); o.converged = true; return; }
-        if (breakdown || o.it >= cfg.max_iters) { copy_vec(x, XC, n, C.s); o.converged = false; return; }
-      }
-      if (j + 1 < R) {
-        k_scale_copy<<<C.vgrid(), TB, 0, C.s>>>(n, W, nrm, V + (int64_t)(j + 1) * n);
-        CK_LAUNCH();
-      }
-    }
-    std::vector<double> y = solve_y(h, R, g, R);
-    C.xupdate(x, R, y, x);
-  }
-}
-
-}  // namespace
+#include "gmres_driver.inc"
 
 extern "C" {
 
-int gdsw_workspace_create(gdsw_workspace** out, int64_t n, int32_t restart) {
-  return guarded([&] {
-    require(restart >= 1, "restart must be at least 1");
-    auto w = std::make_unique<gdsw_workspace>();
-    w->n = n;
-    w->R = restart;
-    w->nblk = 2 * num_sms();
-    const size_t nn = std::max<int64_t>(n, 1);
-    w->V.alloc(nn * (restart + 1));
-    w->Zm.alloc(nn * restart);
-    w->W.alloc(nn);
-    w->MC.alloc(nn);
-    w->ZC.alloc(nn);
-    w->XC.alloc(nn);
-    w->RES.alloc(nn);
-    const int W2 = 2 * (KDOT_ROWS + 1);
-    const int nch = (restart + 1 + KDOT_ROWS - 1) / KDOT_ROWS + 1;
-    w->partial.alloc((size_t)w->nblk * W2);
-    w->dots.alloc((size_t)nch * W2);
-    w->counter.alloc(1);
-    w->counter.zero();
-    CK(cudaDeviceSynchronize());
-    w->coef.alloc(2 * (size_t)restart + 4);
-    w->n_hdots = (size_t)nch * W2;
-    w->n_hcoef = 2 * (size_t)restart + 4;
-    CK(cudaMallocHost(&w->h_dots, w->n_hdots * sizeof(double)));
-    CK(cudaMallocHost(&w->h_coef, w->n_hcoef * sizeof(double)));
-    *out = w.release();
-  });
-}
-
-int gdsw_workspace_destroy(gdsw_workspace* ws) {
-  delete ws;
-  return GDSW_OK;
-}
-
-int gdsw_gmres(const gdsw_csr* a, gdsw_precond* m, const gdsw_csr* m_csr, const double* b, double* x,
-               int x0_nonzero, const gdsw_krylov_cfg* cfg, gdsw_workspace* ws, gdsw_solve_report* rep,
-               double* history, int32_t* true_it, double* true_res, int32_t cap, void* stream) {
-  return guarded([&] {
-    require(a->dtype == GDSW_F64, "GMRES runs on a float64 operator", E_TYPE);
-    require(a->nrows == a->ncols, "operator dimensions do not match the vector");
-    require(ws->n == a->nrows && ws->R >= cfg->restart, "workspace does not match the solve");
-    if (m) require(m->plan->n == a->nrows, "operator dimensions do not match the vector");
-    if (m_csr) require(m_csr->dtype == GDSW_F64 && m_csr->nrows == a->nrows, "operator dimensions do not match the vector");
-    Solver C{a, m, m_csr, b, S(stream), ws, a->nrows};
-    Outcome o;
-    if (cfg->variant == GDSW_SINGLE_REDUCE)
-      gmres_single_reduce(C, x, x0_nonzero != 0, *cfg, o);
-    else
-      gmres_classic(C, x, x0_nonzero != 0, *cfg, o);
-    CK(cudaStreamSynchronize(C.s));
-    rep->iterations = o.it;
-    rep->converged = o.converged ? 1 : 0;
-    rep->iteration_reductions = C.iter_red;
-    rep->residual_reductions = C.res_red;
-    rep->reduction_count = C.iter_red + C.res_red;
-    rep->restarts = o.restarts;
-    rep->n_history = (int32_t)std::min<size_t>(o.history.size(), cap);
-    rep->n_true = (int32_t)std::min<size_t>(o.true_res.size(), cap);
-    for (int k = 0; k < rep->n_history; ++k) history[k] = o.history[k];
-    for (int k = 0; k < rep->n_true; ++k) {
-      true_it[k] = o.true_res[k].first;
-      true_res[k] = o.true_res[k].second;
-    }
-  });
-}
-
-int gdsw_block_dot(const double* V, int64_t ldv, int32_t j, const double* v, const double* z, int64_t n,
-                   double* out, void* stream) {
-  return guarded([&] {
-    require(ldv == n || j == 0, "block_dot expects contiguous rows (ldv == n)");
-    gdsw_workspace ws;
-    ws.n = n;
-    ws.nblk = 2 * num_sms();
-    const int W2 = 2 * (KDOT_ROWS + 1);
-    const int nch = std::max(1, (j + KDOT_ROWS - 1) / KDOT_ROWS);
-    ws.partial.alloc((size_t)ws.nblk * W2);
-    ws.dots.alloc((size_t)nch * W2);
-    ws.counter.alloc(1);
-    ws.counter.zero();
-    CK(cudaDeviceSynchronize());
-    CK(cudaMallocHost(&ws.h_dots, (size_t)nch * W2 * sizeof(double)));
-    Solver C{nullptr, nullptr, nullptr, nullptr, S(stream), &ws, n};
-    std::vector<double> av, az;
-    C.block(V, j, true, v, z, av, az);
-    for (int r = 0; r <= j; ++r) {
-      out[r] = av[r];
-      out[j + 1 + r] = az[r];
-    }
-  });
-}
-
-// ---------------------------------------------------------------------------
 int64_t gdsw_launch_count(void) { return launch_counter().load(); }
 
 int gdsw_prof_enable(int on) {

@@ -1,11 +1,13 @@
 // GMRES vector kernels (krylov.py:260-361 single-reduce, 179-257 classic).
 //
 // * k_block_dot: the ONE fused reduction per single-reduce iteration,
-//   [V[:j]; v]^T [v, z] (krylov.py:290-300). Each thread streams its
-//   elements once, multiplying every basis row against both v and z, so the
-//   block costs one pass over j+2 vectors. Deterministic two-stage reduction
-//   (fixed grid, fixed tree, fixed-order second stage): bitwise
-//   reproducible run to run.
+//   [V[:j]; v]^T [v, z] (krylov.py:290-300). A CTA stages a 1024-element
+//   tile of v and z in shared memory once; its warps then stream the basis
+//   rows of that tile with 16-byte loads (each row read exactly once per
+//   solve pass) against the staged tile. Few rows (norms, MGS dots): several
+//   warps split each row's tile. Deterministic: fixed grid, fixed tile
+//   assignment, fixed shuffle trees, and the last CTA to finish reduces the
+//   per-CTA partials in a fixed order (no second launch).
 // * k_sr_update: v[j], zm[j] and the speculative next candidate w in one
 //   pass (krylov.py:346-351); V[:j] is read once for both a and p/delta.
 #pragma once
@@ -13,59 +15,105 @@
 
 namespace gdsw {
 
-constexpr int KDOT_ROWS = 16;       // basis rows per block-dot launch
+constexpr int KDOT_ROWS = 32;  // rows per block-dot launch (basis rows + self)
 constexpr int KDOT_THREADS = 256;
+constexpr int KDOT_TILE = 1024;
+constexpr int KDOT_W2 = 2 * KDOT_ROWS;
 
-// rows: V[r0 .. r0+nr) (stride ldv) then, if self, the vector v itself.
-// partial[blk][2*(KDOT_ROWS+1)]: [row]*2 + {0: .v, 1: .z}
-__global__ void __launch_bounds__(KDOT_THREADS) k_block_dot(int64_t n, const double* __restrict__ V,
-                                                            int64_t ldv, int nr, int self,
-                                                            const double* __restrict__ v,
-                                                            const double* __restrict__ z,
-                                                            double* __restrict__ partial,
-                                                            double* __restrict__ out,
-                                                            unsigned* __restrict__ counter) {
-  double av[KDOT_ROWS + 1], az[KDOT_ROWS + 1];
-#pragma unroll
-  for (int r = 0; r <= KDOT_ROWS; ++r) av[r] = az[r] = 0.0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const double vi = ldg_stream(v + i);
-    const double zi = z ? ldg_stream(z + i) : 0.0;
-#pragma unroll
-    for (int r = 0; r < KDOT_ROWS; ++r) {
-      if (r < nr) {
-        const double b = ldg_stream(V + r * ldv + i);
-        av[r] = fma(b, vi, av[r]);
-        az[r] = fma(b, zi, az[r]);
-      }
+// rows of the combined list [V[0..nv), v] restricted to [r0, r0 + nrc).
+// out[2*rr + {0,1}] = row . v, row . z  (rr = local row index)
+__global__ void __launch_bounds__(KDOT_THREADS) k_block_dot(
+    int64_t n, const double* __restrict__ V, int64_t ldv, int nv, int r0, int nrc,
+    const double* __restrict__ v, const double* __restrict__ z, double* __restrict__ partial,
+    double* __restrict__ out, unsigned* __restrict__ counter) {
+  __shared__ __align__(16) double sv[KDOT_TILE];
+  __shared__ __align__(16) double sz[KDOT_TILE];
+  __shared__ double red[KDOT_THREADS / 32][4][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NW = KDOT_THREADS / 32;
+  // warps per row (S) when rows are few, else rows per warp (up to 4)
+  const int S = nrc >= 5 ? 1 : (nrc >= 3 ? 2 : (nrc == 2 ? 4 : 8));
+  const int slice = warp % S;
+  const int slice_len = KDOT_TILE / S;
+  const double* rows[4];
+  int nq = 0;
+  if (S > 1) {
+    int rr = warp / S;
+    if (rr < nrc) {
+      int g = r0 + rr;
+      rows[nq++] = g < nv ? V + (int64_t)g * ldv : v;
     }
-    if (self) {
-      av[KDOT_ROWS] = fma(vi, vi, av[KDOT_ROWS]);
-      az[KDOT_ROWS] = fma(vi, zi, az[KDOT_ROWS]);
+  } else {
+    for (int rr = warp; rr < nrc && nq < 4; rr += NW) {
+      int g = r0 + rr;
+      rows[nq++] = g < nv ? V + (int64_t)g * ldv : v;
     }
   }
-  __shared__ double red[KDOT_THREADS / 32][2 * (KDOT_ROWS + 1)];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll
-  for (int r = 0; r <= KDOT_ROWS; ++r) {
-    double a = warp_sum(av[r]);
-    double c = warp_sum(az[r]);
+  double av[4] = {0, 0, 0, 0}, az[4] = {0, 0, 0, 0};
+  const int64_t ntiles = (n + KDOT_TILE - 1) / KDOT_TILE;
+  const bool vec = ((ldv & 1) == 0) && ((reinterpret_cast<uintptr_t>(V) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(v) & 15) == 0);
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t base = tile * KDOT_TILE;
+    const int cnt = (int)(n - base < KDOT_TILE ? n - base : KDOT_TILE);
+    __syncthreads();
+    for (int e = threadIdx.x; e < KDOT_TILE; e += KDOT_THREADS) {
+      sv[e] = e < cnt ? ldg_stream(v + base + e) : 0.0;
+      sz[e] = (z && e < cnt) ? ldg_stream(z + base + e) : 0.0;
+    }
+    __syncthreads();
+    const int e0 = slice * slice_len;
+    for (int q = 0; q < nq; ++q) {
+      const double* row = rows[q] + base;
+      double a = 0.0, c = 0.0;
+      if (vec && cnt == KDOT_TILE) {
+#pragma unroll 4
+        for (int e = e0 + 2 * lane; e < e0 + slice_len; e += 64) {
+          const double2 x = ldg_stream(reinterpret_cast<const double2*>(row + e));
+          const double2 pv = *reinterpret_cast<const double2*>(sv + e);
+          const double2 pz = *reinterpret_cast<const double2*>(sz + e);
+          a = fma(x.x, pv.x, a);
+          a = fma(x.y, pv.y, a);
+          c = fma(x.x, pz.x, c);
+          c = fma(x.y, pz.y, c);
+        }
+      } else {
+        for (int e = e0 + lane; e < e0 + slice_len; e += 32) {
+          if (e < cnt) {
+            const double x = row[e];
+            a = fma(x, sv[e], a);
+            c = fma(x, sz[e], c);
+          }
+        }
+      }
+      av[q] += a;
+      az[q] += c;
+    }
+  }
+  for (int q = 0; q < 4; ++q) {
+    double a = warp_sum(av[q]);
+    double c = warp_sum(az[q]);
     if (lane == 0) {
-      red[warp][2 * r] = a;
-      red[warp][2 * r + 1] = c;
+      red[warp][q][0] = a;
+      red[warp][q][1] = c;
     }
   }
   __syncthreads();
-  constexpr int W2 = 2 * (KDOT_ROWS + 1);
-  for (int k = threadIdx.x; k < W2; k += blockDim.x) {
-    double s = 0.0;
-    for (int w = 0; w < KDOT_THREADS / 32; ++w) s += red[w][k];
-    partial[(int64_t)blockIdx.x * W2 + k] = s;
+  for (int rr = threadIdx.x; rr < nrc; rr += KDOT_THREADS) {
+    double a = 0.0, c = 0.0;
+    if (S > 1) {
+      for (int w = rr * S; w < rr * S + S; ++w) {
+        a += red[w][0][0];
+        c += red[w][0][1];
+      }
+    } else {
+      a = red[rr % NW][rr / NW][0];
+      c = red[rr % NW][rr / NW][1];
+    }
+    partial[(int64_t)blockIdx.x * KDOT_W2 + 2 * rr] = a;
+    partial[(int64_t)blockIdx.x * KDOT_W2 + 2 * rr + 1] = c;
   }
-  // last block to finish reduces all block partials in a fixed order (one
-  // warp per value, lanes strided over blocks, fixed shuffle tree): the
-  // second stage costs no extra launch and stays deterministic
+  // the last CTA reduces all per-CTA partials in a fixed order
   __shared__ bool last;
   __threadfence();
   __syncthreads();
@@ -73,50 +121,93 @@ __global__ void __launch_bounds__(KDOT_THREADS) k_block_dot(int64_t n, const dou
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int k = warp; k < W2; k += KDOT_THREADS / 32) {
+  for (int k = warp; k < 2 * nrc; k += NW) {
     double s = 0.0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(partial + (int64_t)b * W2 + k);
+    for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(partial + (int64_t)b * KDOT_W2 + k);
     s = warp_sum(s);
     if (lane == 0) out[k] = s;
   }
   if (threadIdx.x == 0) *counter = 0u;
 }
 
-// out[k] = sum over blocks (ascending) of partial[blk][k]
-__global__ void k_reduce_partials(int nblk, int width, const double* __restrict__ partial,
-                                  double* __restrict__ out) {
-  int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= width) return;
-  double s = 0.0;
-  for (int b = 0; b < nblk; ++b) s += partial[(int64_t)b * width + k];
-  out[k] = s;
-}
-
-// single-reduce update (krylov.py:346-351). coef = [a(0..j), pd(0..j)],
-// pd = p / delta.
+// single-reduce update (krylov.py:346-351). coef = [a(0..j), p/delta(0..j),
+// delta, corr]. VW = 2: 16-byte vector path (rows of even ld, aligned).
+template <int VW>
 __global__ void __launch_bounds__(256) k_sr_update(int64_t n, double* __restrict__ V,
                                                    double* __restrict__ Zm, int64_t ld, int j,
-                                                   const double* __restrict__ coef, double delta,
-                                                   double corr, double* __restrict__ W,
+                                                   const double* __restrict__ coef,
+                                                   double* __restrict__ W,
                                                    const double* __restrict__ Mc,
                                                    const double* __restrict__ Zc) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    double va = 0.0, wp = 0.0, za = 0.0;
-    for (int r = 0; r < j; ++r) {
-      const double vr = ldg_stream(V + r * ld + i);
-      const double zr = ldg_stream(Zm + r * ld + i);
-      const double a = __ldg(coef + r), pd = __ldg(coef + j + r);
-      va = fma(a, vr, va);
-      wp = fma(pd, vr, wp);
-      za = fma(a, zr, za);
+  const double delta = coef[2 * j], corr = coef[2 * j + 1];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * VW;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * VW; i < n; i += stride) {
+    if (VW == 2 && i + 1 < n) {
+      double2 va = {0, 0}, wp = {0, 0}, za = {0, 0};
+#pragma unroll 4
+      for (int r = 0; r < j; ++r) {
+        const double2 vr = ldg_stream(reinterpret_cast<const double2*>(V + r * ld + i));
+        const double2 zr = ldg_stream(reinterpret_cast<const double2*>(Zm + r * ld + i));
+        const double a = __ldg(coef + r), pd = __ldg(coef + j + r);
+        va.x = fma(a, vr.x, va.x);
+        va.y = fma(a, vr.y, va.y);
+        wp.x = fma(pd, vr.x, wp.x);
+        wp.y = fma(pd, vr.y, wp.y);
+        za.x = fma(a, zr.x, za.x);
+        za.y = fma(a, zr.y, za.y);
+      }
+      const double2 w = *reinterpret_cast<const double2*>(W + i);
+      const double2 mc = ldg_stream(reinterpret_cast<const double2*>(Mc + i));
+      const double2 zc = ldg_stream(reinterpret_cast<const double2*>(Zc + i));
+      double2 vj, zj, wn;
+      vj.x = (w.x - va.x) / delta;
+      vj.y = (w.y - va.y) / delta;
+      zj.x = (mc.x - za.x) / delta;
+      zj.y = (mc.y - za.y) / delta;
+      wn.x = zc.x / delta - wp.x - corr * vj.x;
+      wn.y = zc.y / delta - wp.y - corr * vj.y;
+      __stcs(reinterpret_cast<double2*>(V + (int64_t)j * ld + i), vj);
+      __stcs(reinterpret_cast<double2*>(Zm + (int64_t)j * ld + i), zj);
+      *reinterpret_cast<double2*>(W + i) = wn;
+    } else {
+      const int64_t kend = i + VW < n ? i + VW : n;
+      for (int64_t k = i; k < kend; ++k) {
+        double va = 0.0, wp = 0.0, za = 0.0;
+        for (int r = 0; r < j; ++r) {
+          const double vr = V[r * ld + k], zr = Zm[r * ld + k];
+          va = fma(coef[r], vr, va);
+          wp = fma(coef[j + r], vr, wp);
+          za = fma(coef[r], zr, za);
+        }
+        const double vj = (W[k] - va) / delta;
+        V[(int64_t)j * ld + k] = vj;
+        Zm[(int64_t)j * ld + k] = (Mc[k] - za) / delta;
+        W[k] = Zc[k] / delta - wp - corr * vj;
+      }
     }
-    const double vj = (W[i] - va) / delta;
-    const double zj = (Mc[i] - za) / delta;
-    V[(int64_t)j * ld + i] = vj;
-    Zm[(int64_t)j * ld + i] = zj;
-    W[i] = Zc[i] / delta - wp - corr * vj;
   }
+}
+
+// device-side single-reduce scalars from the fused block (krylov.py:305-306,
+// 346-350), same operation order as the host copy: lets the next update be
+// enqueued before the host has read the block back.
+// blk: [a(0..j), b2] .v column at even slots, [p, q] at odd slots
+__global__ void k_sr_coef(int j, const double* __restrict__ blk, double* __restrict__ coef) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double aa = 0.0, ap = 0.0;
+  for (int r = 0; r < j; ++r) {
+    const double a = blk[2 * r], p = blk[2 * r + 1];
+    aa = rn_add(aa, rn_mul(a, a));
+    ap = rn_add(ap, rn_mul(a, p));
+  }
+  const double d2 = rn_sub(blk[2 * j], aa);
+  const double delta = d2 > 0.0 ? sqrt(d2) : 0.0;
+  for (int r = 0; r < j; ++r) {
+    coef[r] = blk[2 * r];
+    coef[j + r] = rn_div(blk[2 * r + 1], delta);
+  }
+  coef[2 * j] = delta;
+  coef[2 * j + 1] = rn_div(rn_sub(blk[2 * j + 1], ap), rn_mul(delta, delta));
 }
 
 // x_out = x + sum_r y[r] Zm[r]   (krylov.py:340, 361)
@@ -127,13 +218,13 @@ __global__ void __launch_bounds__(256) k_x_update(int64_t n, const double* __res
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     double acc = 0.0;
+#pragma unroll 4
     for (int r = 0; r < m; ++r) acc = fma(__ldg(y + r), ldg_stream(Zm + r * ld + i), acc);
     xo[i] = x[i] + acc;
   }
 }
 
-// classic Arnoldi helpers (krylov.py:217-236): w -= sum_r h[r] v[r]; and
-// v_out = w / nrm
+// classic Arnoldi helpers (krylov.py:217-236): w -= sum_r h[r] v[r]
 __global__ void __launch_bounds__(256) k_multi_axpy(int64_t n, const double* __restrict__ V,
                                                     int64_t ld, int m,
                                                     const double* __restrict__ h,
