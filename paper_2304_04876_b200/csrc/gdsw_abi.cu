@@ -54,6 +54,27 @@ std::vector<int64_t> vec(const int64_t* p, size_t n) {
 }
 
 constexpr int TB = 256;
+
+// GDSW_JACOBI_FUSED=1 selects the cluster-fused FastSpTRSV (one launch,
+// factors L2-resident); default is one launch per sweep, measured faster
+// on B200 until the fused kernel's latency chain is shortened
+// GDSW_L2HINT=1 enables L2 evict_last hints on the Jacobi iterates
+// (measured slower on B200 at C2: off by default)
+bool l2_hints_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GDSW_L2HINT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+bool jacobi_fused_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("GDSW_JACOBI_FUSED");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 }  // namespace
 
 // ===========================================================================
@@ -526,7 +547,7 @@ struct gdsw_precond {
   DBuf<double> panel64;
   DBuf<char> panel32;              // f32 copy when dtype == F32
   DBuf<char> pgr_val, pgt_val, ainv;
-  DBuf<char> xb, x1, x2, pdot, cu, cv;
+  DBuf<char> xb, x1, x2, x3, pdot, cu, cv;
   std::mutex mu;
   cudaEvent_t last = nullptr;
   ~gdsw_precond() {
@@ -564,7 +585,7 @@ namespace {
 
 // FastSpTRSV: `iters` Jacobi iterates on L then U; returns the buffer
 // holding the block solutions
-template <typename T>
+template <typename T, bool HINT>
 T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   gdsw_plan* P = m->plan;
   const int32_t n = (int32_t)P->n_loc;
@@ -575,6 +596,20 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   const unsigned g = grid_for(n, TB);
   const double lbytes = (double)P->nnz_l * (sizeof(T) + 4) + n * (2.0 + 3 * sizeof(T));
   const double ubytes = (double)(P->nnz_u - n) * (sizeof(T) + 4) + n * (2.0 + 3 * sizeof(T));
+  if (jacobi_fused_enabled() && iters >= 1) {
+    // one cluster per subdomain, all iterates in one launch. Algorithmic
+    // bytes: both factors once (SELL values + columns + row lengths), U's
+    // diagonal, the gather (gmap + r) and the result; iterates stay in L2.
+    const double bytes = (double)P->nnz_l * (sizeof(T) + 4) + (double)(P->nnz_u - n) * (sizeof(T) + 4) +
+                         n * (2.0 * 2 + sizeof(T)) + n * 12.0 + n * (double)sizeof(T);
+    ProfScope ps("jacobi_fused", s, bytes);
+    JacobiClusterDev J{L, U, P->sub_ptr.p, P->gmap.p, iters};
+    k_jacobi_cluster<T><<<P->n_sub * JC_CLUSTER, JC_THREADS, 0, s>>>(
+        J, (const T*)m->lsell.p, (const T*)m->usell.p, (const T*)m->udiag.p, r, B, X1, X2);
+    CK_LAUNCH();
+    T* bufs[3] = {B, X1, X2};
+    return bufs[jc_result_buffer(iters)];
+  }
   // algorithmic bytes per launch: SELL values+columns once, row lengths,
   // b and x read once (gathers assumed cached), x_new written; the gather
   // variant reads r through gmap (4 + 8 per row, twice for the neighbours'
@@ -588,16 +623,36 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   } else {
     {
       ProfScope ps("gather_jacobi_lower", s, lbytes + n * (12.0 - sizeof(T)));
-      k_gather_jacobi_lower<T><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, P->gmap.p, r, B, X1);
+      k_gather_jacobi_lower<T, HINT><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, P->gmap.p, r, B, X1);
       CK_LAUNCH();
     }
     T* cur = X1;
     T* oth = X2;
-    for (int t = 2; t < iters; ++t) {
+    for (int t = 2; t < iters - 1; ++t) {
       ProfScope ps("jacobi_lower", s, lbytes);
-      k_jacobi_lower<T><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth);
+      k_jacobi_lower<T, HINT><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth);
       CK_LAUNCH();
       std::swap(cur, oth);
+    }
+    if (iters >= 3) {
+      // last L iterate fused with U's first iterate y1 = F / diag
+      T* X3 = (T*)m->x3.p;
+      {
+        ProfScope ps("jacobi_lower_diag", s, lbytes + n * 2.0 * sizeof(T));
+        k_jacobi_lower_diag<T, HINT><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth,
+                                                (const T*)m->udiag.p, X3);
+        CK_LAUNCH();
+      }
+      F = oth;
+      T* Gf = X3;
+      T* Hf = cur;  // B and cur are free now
+      for (int t = 1; t < iters; ++t) {
+        ProfScope ps("jacobi_upper", s, ubytes + n * (double)sizeof(T));
+        k_jacobi_upper<T, HINT><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, Gf, Hf);
+        CK_LAUNCH();
+        std::swap(Gf, Hf);
+      }
+      return Gf;
     }
     F = cur;
   }
@@ -613,7 +668,7 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   T* oth = H;
   for (int t = 1; t < iters; ++t) {
     ProfScope ps("jacobi_upper", s, ubytes + n * (double)sizeof(T));
-    k_jacobi_upper<T><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, cur, oth);
+    k_jacobi_upper<T, HINT><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, cur, oth);
     CK_LAUNCH();
     std::swap(cur, oth);
   }
@@ -635,7 +690,8 @@ T* local_solve(gdsw_precond* m, const double* r, int jacobi_iters, cudaStream_t 
   gdsw_plan* P = m->plan;
   if (jacobi_iters > 0 || P->method == GDSW_FAST_ILU) {
     m->ensure_jacobi();
-    return jacobi_solve<T>(m, r, jacobi_iters > 0 ? jacobi_iters : m->iters, s);
+    const int it = jacobi_iters > 0 ? jacobi_iters : m->iters;
+    return l2_hints_enabled() ? jacobi_solve<T, true>(m, r, it, s) : jacobi_solve<T, false>(m, r, it, s);
   }
   return levelset_solve<T>(m, r, s);
 }
@@ -732,6 +788,7 @@ int gdsw_precond_create(gdsw_precond** out, gdsw_plan* plan, int dtype, int tris
     m->xb.alloc(nl);
     m->x1.alloc(nl);
     m->x2.alloc(nl);
+    m->x3.alloc(nl);
     CK(cudaEventCreateWithFlags(&m->last, cudaEventDisableTiming));
     CK(cudaEventRecord(m->last, 0));
     *out = m.release();

@@ -22,19 +22,18 @@ constexpr int KDOT_W2 = 2 * KDOT_ROWS;
 
 // rows of the combined list [V[0..nv), v] restricted to [r0, r0 + nrc).
 // out[2*rr + {0,1}] = row . v, row . z  (rr = local row index)
-__global__ void __launch_bounds__(KDOT_THREADS) k_block_dot(
+__global__ void __launch_bounds__(KDOT_THREADS, 3) k_block_dot(
     int64_t n, const double* __restrict__ V, int64_t ldv, int nv, int r0, int nrc,
     const double* __restrict__ v, const double* __restrict__ z, double* __restrict__ partial,
     double* __restrict__ out, unsigned* __restrict__ counter) {
-  __shared__ __align__(16) double sv[KDOT_TILE];
-  __shared__ __align__(16) double sz[KDOT_TILE];
   __shared__ double red[KDOT_THREADS / 32][4][2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NW = KDOT_THREADS / 32;
-  // warps per row (S) when rows are few, else rows per warp (up to 4)
+  constexpr int KT = 256;      // elements per warp tile: 4 x 16-byte loads per lane
+  // S warps per row when rows are few (each on its own tiles), else up to 4
+  // rows per warp (all warps of the CTA on the same tile, v/z hit L1)
   const int S = nrc >= 5 ? 1 : (nrc >= 3 ? 2 : (nrc == 2 ? 4 : 8));
   const int slice = warp % S;
-  const int slice_len = KDOT_TILE / S;
   const double* rows[4];
   int nq = 0;
   if (S > 1) {
@@ -50,44 +49,50 @@ __global__ void __launch_bounds__(KDOT_THREADS) k_block_dot(
     }
   }
   double av[4] = {0, 0, 0, 0}, az[4] = {0, 0, 0, 0};
-  const int64_t ntiles = (n + KDOT_TILE - 1) / KDOT_TILE;
+  const int64_t ntiles = (n + KT - 1) / KT;
   const bool vec = ((ldv & 1) == 0) && ((reinterpret_cast<uintptr_t>(V) & 15) == 0) &&
-                   ((reinterpret_cast<uintptr_t>(v) & 15) == 0);
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t base = tile * KDOT_TILE;
-    const int cnt = (int)(n - base < KDOT_TILE ? n - base : KDOT_TILE);
-    __syncthreads();
-    for (int e = threadIdx.x; e < KDOT_TILE; e += KDOT_THREADS) {
-      sv[e] = e < cnt ? ldg_stream(v + base + e) : 0.0;
-      sz[e] = (z && e < cnt) ? ldg_stream(z + base + e) : 0.0;
-    }
-    __syncthreads();
-    const int e0 = slice * slice_len;
-    for (int q = 0; q < nq; ++q) {
-      const double* row = rows[q] + base;
-      double a = 0.0, c = 0.0;
-      if (vec && cnt == KDOT_TILE) {
-#pragma unroll 4
-        for (int e = e0 + 2 * lane; e < e0 + slice_len; e += 64) {
-          const double2 x = ldg_stream(reinterpret_cast<const double2*>(row + e));
-          const double2 pv = *reinterpret_cast<const double2*>(sv + e);
-          const double2 pz = *reinterpret_cast<const double2*>(sz + e);
-          a = fma(x.x, pv.x, a);
-          a = fma(x.y, pv.y, a);
-          c = fma(x.x, pz.x, c);
-          c = fma(x.y, pz.y, c);
-        }
-      } else {
-        for (int e = e0 + lane; e < e0 + slice_len; e += 32) {
-          if (e < cnt) {
-            const double x = row[e];
-            a = fma(x, sv[e], a);
-            c = fma(x, sz[e], c);
-          }
-        }
+                   ((reinterpret_cast<uintptr_t>(v) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(z) & 15) == 0);
+  for (int64_t t0 = (int64_t)blockIdx.x * S; t0 < ntiles; t0 += (int64_t)gridDim.x * S) {
+    const int64_t tile = t0 + slice;
+    if (tile >= ntiles || nq == 0) continue;
+    const int64_t base = tile * KT;
+    const int cnt = (int)(n - base < KT ? n - base : KT);
+    if (vec && cnt == KT) {
+      double2 pv[4], pz[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int64_t e = base + 64 * t + 2 * lane;
+        pv[t] = __ldg(reinterpret_cast<const double2*>(v + e));
+        pz[t] = z ? __ldg(reinterpret_cast<const double2*>(z + e)) : make_double2(0.0, 0.0);
       }
-      av[q] += a;
-      az[q] += c;
+      for (int q = 0; q < nq; ++q) {
+        double2 x[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          x[t] = ldg_stream(reinterpret_cast<const double2*>(rows[q] + base + 64 * t + 2 * lane));
+        double a = 0.0, c = 0.0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          a = fma(x[t].x, pv[t].x, a);
+          a = fma(x[t].y, pv[t].y, a);
+          c = fma(x[t].x, pz[t].x, c);
+          c = fma(x[t].y, pz[t].y, c);
+        }
+        av[q] += a;
+        az[q] += c;
+      }
+    } else {
+      for (int q = 0; q < nq; ++q) {
+        double a = 0.0, c = 0.0;
+        for (int e = lane; e < cnt; e += 32) {
+          const double x = rows[q][base + e];
+          a = fma(x, v[base + e], a);
+          if (z) c = fma(x, z[base + e], c);
+        }
+        av[q] += a;
+        az[q] += c;
+      }
     }
   }
   for (int q = 0; q < 4; ++q) {

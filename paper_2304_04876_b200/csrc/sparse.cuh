@@ -91,6 +91,50 @@ __global__ void k_csr_to_sell(int32_t n, const int64_t* __restrict__ ptr,
 }
 
 // ---------------------------------------------------------------------------
+// one SELL row, entries consumed in column order, loads issued SELL_U at a
+// time: {columns, values} for SELL_U entries together, then the SELL_U x
+// gathers together, then the ordered accumulation -- the dependent-load
+// chain per row drops from 2*len round trips to 2*ceil(len/SELL_U)
+// ---------------------------------------------------------------------------
+constexpr int SELL_U = 4;
+
+struct LdNc {  // read-only for the whole kernel: non-coherent path
+  template <typename T>
+  __device__ __forceinline__ static T ld(const T* p) { return __ldg(p); }
+};
+struct LdCg {  // written by other CTAs of the same kernel: L2 only
+  template <typename T>
+  __device__ __forceinline__ static T ld(const T* p) { return __ldcg(p); }
+};
+
+// SUB: acc -= v*x (triangular sweeps); else acc += v*x (SpMV)
+template <typename T, typename TX, bool SUB, typename XL>
+__device__ __forceinline__ T sell_row(T acc, int64_t base, int len, const T* __restrict__ val,
+                                      const int32_t* __restrict__ col, const TX* x) {
+  for (int k0 = 0; k0 < len; k0 += SELL_U) {
+    int32_t c[SELL_U];
+    T v[SELL_U];
+#pragma unroll
+    for (int u = 0; u < SELL_U; ++u) {
+      if (k0 + u < len) {
+        const int64_t q = base + 32 * (int64_t)(k0 + u);
+        c[u] = ldg_stream(col + q);
+        v[u] = ldg_stream(val + q);
+      }
+    }
+    T xv[SELL_U];
+#pragma unroll
+    for (int u = 0; u < SELL_U; ++u)
+      if (k0 + u < len) xv[u] = (T)XL::ld(x + c[u]);
+#pragma unroll
+    for (int u = 0; u < SELL_U; ++u) {
+      if (k0 + u < len) acc = SUB ? rn_sub(acc, rn_mul(v[u], xv[u])) : rn_add(acc, rn_mul(v[u], xv[u]));
+    }
+  }
+  return acc;
+}
+
+// ---------------------------------------------------------------------------
 // SpMV: y = A x (mode 0), y = yin - A x (mode 1), y = alpha A x + beta yin (2)
 // ---------------------------------------------------------------------------
 template <typename T>
@@ -102,25 +146,7 @@ __global__ void __launch_bounds__(256) k_sell_spmv(SellDev A, const T* __restric
   if (i >= A.n_rows) return;
   const int64_t base = A.slice_off[i >> 5] + (i & 31);
   const int len = A.row_len[i];
-  T acc = T(0);
-  int k = 0;
-  // 4 independent loads in flight per thread before the dependent gathers
-  for (; k + 4 <= len; k += 4) {
-    const int64_t q = base + 32 * (int64_t)k;
-    int32_t c0 = ldg_stream(A.col + q), c1 = ldg_stream(A.col + q + 32);
-    int32_t c2 = ldg_stream(A.col + q + 64), c3 = ldg_stream(A.col + q + 96);
-    T v0 = ldg_stream(val + q), v1 = ldg_stream(val + q + 32);
-    T v2 = ldg_stream(val + q + 64), v3 = ldg_stream(val + q + 96);
-    T x0 = __ldg(x + c0), x1 = __ldg(x + c1), x2 = __ldg(x + c2), x3 = __ldg(x + c3);
-    acc = rn_add(acc, rn_mul(v0, x0));
-    acc = rn_add(acc, rn_mul(v1, x1));
-    acc = rn_add(acc, rn_mul(v2, x2));
-    acc = rn_add(acc, rn_mul(v3, x3));
-  }
-  for (; k < len; ++k) {
-    const int64_t q = base + 32 * (int64_t)k;
-    acc = rn_add(acc, rn_mul(ldg_stream(val + q), __ldg(x + ldg_stream(A.col + q))));
-  }
+  const T acc = sell_row<T, T, false, LdNc>(T(0), base, len, val, A.col, x);
   if (mode == 0) {
     y[i] = acc;
   } else if (mode == 1) {
@@ -136,25 +162,38 @@ __global__ void __launch_bounds__(256) k_sell_spmv(SellDev A, const T* __restric
 // (jacobi_trisolve_lower_unit / _upper, _kernels.py:620-656)
 // ---------------------------------------------------------------------------
 // x_new = b - (L - I) x      (L strict lower in SELL)
-template <typename T>
+// HINT: iterate vectors read/written with L2 evict_last (they are re-read by
+// the next sweep), factor values stream with evict_first
+template <typename T, bool HINT>
+struct VecIO {
+  uint64_t pol;
+  __device__ __forceinline__ VecIO() : pol(HINT ? l2_policy_last() : 0) {}
+  __device__ __forceinline__ T ld(const T* p) const { return HINT ? ld_last(p, pol) : *p; }
+  __device__ __forceinline__ void st(T* p, T v) const {
+    if (HINT) st_last(p, v, pol); else *p = v;
+  }
+};
+
+template <typename T, bool HINT>
 __global__ void __launch_bounds__(256) k_jacobi_lower(SellDev L, const T* __restrict__ lval,
                                                       const T* __restrict__ b,
                                                       const T* __restrict__ x,
                                                       T* __restrict__ xn) {
   int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= L.n_rows) return;
+  const VecIO<T, HINT> io;
   const int64_t base = L.slice_off[i >> 5] + (i & 31);
   const int len = L.row_len[i];
-  T acc = b[i];
+  T acc = io.ld(b + i);
   for (int k = 0; k < len; ++k) {
     const int64_t q = base + 32 * (int64_t)k;
-    acc = rn_sub(acc, rn_mul(ldg_stream(lval + q), x[ldg_stream(L.col + q)]));
+    acc = rn_sub(acc, rn_mul(ldg_stream(lval + q), io.ld(x + ldg_stream(L.col + q))));
   }
-  xn[i] = acc;
+  io.st(xn + i, acc);
 }
 
 // x_new = D^-1 (b - (U - D) x)  (U off-diagonal part in SELL, D separate)
-template <typename T>
+template <typename T, bool HINT>
 __global__ void __launch_bounds__(256) k_jacobi_upper(SellDev U, const T* __restrict__ uval,
                                                       const T* __restrict__ diag,
                                                       const T* __restrict__ b,
@@ -162,14 +201,38 @@ __global__ void __launch_bounds__(256) k_jacobi_upper(SellDev U, const T* __rest
                                                       T* __restrict__ xn) {
   int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= U.n_rows) return;
+  const VecIO<T, HINT> io;
   const int64_t base = U.slice_off[i >> 5] + (i & 31);
   const int len = U.row_len[i];
-  T acc = b[i];
+  T acc = io.ld(b + i);
   for (int k = 0; k < len; ++k) {
     const int64_t q = base + 32 * (int64_t)k;
-    acc = rn_sub(acc, rn_mul(ldg_stream(uval + q), x[ldg_stream(U.col + q)]));
+    acc = rn_sub(acc, rn_mul(ldg_stream(uval + q), io.ld(x + ldg_stream(U.col + q))));
   }
-  xn[i] = rn_div(acc, diag[i]);
+  io.st(xn + i, rn_div(acc, io.ld(diag + i)));
+}
+
+// last L sweep fused with the first U iterate: writes both the L result F
+// and y1 = F / diag (saves one pass over the vectors)
+template <typename T, bool HINT>
+__global__ void __launch_bounds__(256) k_jacobi_lower_diag(SellDev L, const T* __restrict__ lval,
+                                                           const T* __restrict__ b,
+                                                           const T* __restrict__ x,
+                                                           T* __restrict__ xn,
+                                                           const T* __restrict__ diag,
+                                                           T* __restrict__ y1) {
+  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= L.n_rows) return;
+  const VecIO<T, HINT> io;
+  const int64_t base = L.slice_off[i >> 5] + (i & 31);
+  const int len = L.row_len[i];
+  T f = io.ld(b + i);
+  for (int k = 0; k < len; ++k) {
+    const int64_t q = base + 32 * (int64_t)k;
+    f = rn_sub(f, rn_mul(ldg_stream(lval + q), io.ld(x + ldg_stream(L.col + q))));
+  }
+  io.st(xn + i, f);
+  io.st(y1 + i, rn_div(f, io.ld(diag + i)));
 }
 
 template <typename T>
@@ -190,7 +253,7 @@ __global__ void k_gather(int32_t n, const int32_t* __restrict__ gmap, const doub
 
 // gather fused with the first Jacobi L sweep: writes b = T(r[gmap]) and the
 // second iterate b - (L - I) b in one pass over L
-template <typename T>
+template <typename T, bool HINT>
 __global__ void __launch_bounds__(256) k_gather_jacobi_lower(SellDev L,
                                                              const T* __restrict__ lval,
                                                              const int32_t* __restrict__ gmap,
@@ -201,13 +264,155 @@ __global__ void __launch_bounds__(256) k_gather_jacobi_lower(SellDev L,
   if (i >= L.n_rows) return;
   const int64_t base = L.slice_off[i >> 5] + (i & 31);
   const int len = L.row_len[i];
-  T acc = (T)r[gmap[i]];
-  b[i] = acc;
-  for (int k = 0; k < len; ++k) {
-    const int64_t q = base + 32 * (int64_t)k;
-    acc = rn_sub(acc, rn_mul(ldg_stream(lval + q), (T)r[__ldg(gmap + ldg_stream(L.col + q))]));
+  const VecIO<T, HINT> io;
+  const T bi = (T)r[gmap[i]];
+  io.st(b + i, bi);
+  // x1 = b: neighbours' b read straight from r through gmap
+  T acc = bi;
+  for (int k0 = 0; k0 < len; k0 += SELL_U) {
+    int32_t c[SELL_U];
+    T v[SELL_U];
+#pragma unroll
+    for (int u = 0; u < SELL_U; ++u) {
+      if (k0 + u < len) {
+        const int64_t q = base + 32 * (int64_t)(k0 + u);
+        c[u] = ldg_stream(L.col + q);
+        v[u] = ldg_stream(lval + q);
+      }
+    }
+    int32_t g[SELL_U];
+#pragma unroll
+    for (int u = 0; u < SELL_U; ++u)
+      if (k0 + u < len) g[u] = __ldg(gmap + c[u]);
+#pragma unroll
+    for (int u = 0; u < SELL_U; ++u)
+      if (k0 + u < len) acc = rn_sub(acc, rn_mul(v[u], (T)__ldg(r + g[u])));
   }
-  xn[i] = acc;
+  io.st(xn + i, acc);
+}
+
+// ---------------------------------------------------------------------------
+// Cluster-fused FastSpTRSV: one thread-block cluster per subdomain runs the
+// gather and ALL Jacobi iterates of L and U in one launch, with a cluster
+// barrier between iterates. While a cluster works on its subdomain, that
+// subdomain's factors (~3 MB) and iterates (~1 MB) stay in L2, so only the
+// first sweep of each factor streams from HBM (18 clusters of 8 CTAs are
+// resident at once: ~60 MB of L2). Per-row arithmetic is unchanged
+// (bit-identical to jacobi_trisolve_*); iterate reads go through L2
+// (ld.global.cg) because other CTAs of the cluster wrote them.
+// ---------------------------------------------------------------------------
+constexpr int JC_CLUSTER = 8;
+constexpr int JC_THREADS = 1024;
+
+struct JacobiClusterDev {
+  SellDev L, U;
+  const int32_t* sub_ptr;
+  const int32_t* gmap;
+  int iters;
+};
+
+__device__ __forceinline__ void cluster_barrier() {
+  __threadfence();
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+
+// JC_ILP rows per thread per step, all their loads in flight together (the
+// per-row accumulation order is untouched)
+constexpr int JC_ILP = 4;
+
+template <typename T, bool UPPER>
+__device__ __forceinline__ void jc_rows(const SellDev& M, const T* __restrict__ val,
+                                        const T* __restrict__ diag, const T* b, const T* x, T* xn,
+                                        int32_t lo, int32_t a0, int32_t hi) {
+  for (int32_t i0 = a0 + threadIdx.x; i0 < hi; i0 += JC_ILP * blockDim.x) {
+    T acc[JC_ILP];
+#pragma unroll
+    for (int m = 0; m < JC_ILP; ++m) {
+      const int32_t i = i0 + m * blockDim.x;
+      const bool ok = i < hi && i >= lo;
+      const int32_t ic = ok ? i : lo;
+      const int64_t base = M.slice_off[ic >> 5] + (ic & 31);
+      const int len = ok ? M.row_len[ic] : 0;
+      acc[m] = sell_row<T, T, true, LdCg>(ok ? __ldcg(b + ic) : T(0), base, len, val, M.col, x);
+    }
+#pragma unroll
+    for (int m = 0; m < JC_ILP; ++m) {
+      const int32_t i = i0 + m * blockDim.x;
+      if (i < hi && i >= lo) xn[i] = UPPER ? rn_div(acc[m], diag[i]) : acc[m];
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void jc_lower_rows(const SellDev& L, const T* __restrict__ lval,
+                                              const T* b, const T* x, T* xn, int32_t lo,
+                                              int32_t a0, int32_t hi) {
+  jc_rows<T, false>(L, lval, nullptr, b, x, xn, lo, a0, hi);
+}
+
+template <typename T>
+__device__ __forceinline__ void jc_upper_rows(const SellDev& U, const T* __restrict__ uval,
+                                              const T* __restrict__ diag, const T* b, const T* x,
+                                              T* xn, int32_t lo, int32_t a0, int32_t hi) {
+  jc_rows<T, true>(U, uval, diag, b, x, xn, lo, a0, hi);
+}
+
+// the buffer rotation (shared with the host, which needs the result buffer)
+__host__ __device__ inline int jc_result_buffer(int iters) {
+  // buffers: 0 = B, 1 = X1, 2 = X2 ; returns the buffer holding the U result
+  int F = 0;
+  if (iters >= 2) {
+    int cur = 1, oth = 2;
+    for (int t = 2; t < iters; ++t) { int tmp = cur; cur = oth; oth = tmp; }
+    F = cur;
+  }
+  int G = (F == 0) ? 1 : 0, H = (F == 2) ? 1 : 2;
+  if (F == 1) { G = 0; H = 2; }
+  int cur = G, oth = H;
+  for (int t = 1; t < iters; ++t) { int tmp = cur; cur = oth; oth = tmp; }
+  return cur;
+}
+
+template <typename T>
+__global__ void __cluster_dims__(JC_CLUSTER, 1, 1) __launch_bounds__(JC_THREADS, 1)
+    k_jacobi_cluster(JacobiClusterDev P, const T* __restrict__ lval, const T* __restrict__ uval,
+                     const T* __restrict__ diag, const double* __restrict__ r, T* B, T* X1, T* X2) {
+  const int s = blockIdx.x / JC_CLUSTER;
+  const int rank = blockIdx.x % JC_CLUSTER;
+  const int32_t lo = P.sub_ptr[s], hi = P.sub_ptr[s + 1];
+  // this CTA's slice-aligned share of the subdomain's rows
+  const int32_t alo = lo & ~31;
+  const int32_t piece = (((hi - alo + JC_CLUSTER - 1) / JC_CLUSTER) + 31) & ~31;
+  const int32_t a0 = alo + rank * piece;
+  const int32_t my_hi = min(hi, a0 + piece);
+  T* buf[3] = {B, X1, X2};
+  for (int32_t i = a0 + threadIdx.x; i < my_hi; i += blockDim.x)
+    if (i >= lo) B[i] = (T)r[P.gmap[i]];
+  cluster_barrier();
+  int F = 0;
+  if (P.iters >= 2) {
+    jc_lower_rows<T>(P.L, lval, B, B, X1, lo, a0, my_hi);
+    cluster_barrier();
+    int cur = 1, oth = 2;
+    for (int t = 2; t < P.iters; ++t) {
+      jc_lower_rows<T>(P.L, lval, B, buf[cur], buf[oth], lo, a0, my_hi);
+      cluster_barrier();
+      int tmp = cur; cur = oth; oth = tmp;
+    }
+    F = cur;
+  }
+  int G = (F == 0) ? 1 : 0, H = (F == 2) ? 1 : 2;
+  if (F == 1) { G = 0; H = 2; }
+  for (int32_t i = a0 + threadIdx.x; i < my_hi; i += blockDim.x)
+    if (i >= lo) buf[G][i] = rn_div(buf[F][i], diag[i]);
+  cluster_barrier();
+  int cur = G, oth = H;
+  for (int t = 1; t < P.iters; ++t) {
+    jc_upper_rows<T>(P.U, uval, diag, buf[F], buf[cur], buf[oth], lo, a0, my_hi);
+    cluster_barrier();
+    int tmp = cur; cur = oth; oth = tmp;
+  }
 }
 
 // ---------------------------------------------------------------------------
