@@ -107,6 +107,24 @@ def workload(args) -> dict:
                   "vectors ~1.9 GB) >> 126 MB L2"}
 
 
+PHASE_KERNEL = {"jacobi_upper": "k_jacobi_upper", "jacobi_lower": "k_jacobi_lower",
+                "sr_update": "k_sr_update", "block_dot": "k_block_dot",
+                "restrict_panels": "k_restrict_chunks", "prolong_interior": "k_prolong_interior",
+                "spmv": "k_sell_spmv", "jacobi_fused": "k_jacobi_cluster"}
+
+
+def ncu_traffic(phase: str):
+    """DRAM read+write bytes per launch of the phase's kernel from the
+    committed `ncu --set full` capture summary (profiles/*_ncu_summary.json),
+    or None when no capture of that kernel exists."""
+    kern = PHASE_KERNEL.get(phase)
+    for f in sorted((ROOT / "profiles").glob("*_ncu_summary.json"), reverse=True):
+        for c in json.loads(f.read_text()).get("captures", []):
+            if c.get("kernel") == kern and c.get("traffic_bytes"):
+                return {"bytes": c["traffic_bytes"], "source": f"profiles/{f.name}:{c['capture']}"}
+    return None
+
+
 def peaks():
     f = ROOT / "MEASURED_PEAKS.json"
     if f.exists():
@@ -274,8 +292,12 @@ def native(args):
         "solve_gbs": step_bytes / (solve_ms * 1e-3) / 1e9,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": d["gbs"], "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": d["gbs"] / peak,
-                     "traffic": None, "us_per_launch": d["us_per_launch"],
-                     "bytes_per_launch": d["bytes_per_launch"]},
+                     "traffic": (ncu_traffic(dom) or {}).get("bytes"),
+                     "traffic_source": (ncu_traffic(dom) or {}).get("source"),
+                     "us_per_launch": d["us_per_launch"],
+                     "bytes_per_launch": d["bytes_per_launch"],
+                     "timing": "libgdsw CUDA events on the launching stream, K-solve pass "
+                               "identical to the timed one"},
         "phases": {k: {kk: round(vv, 4) for kk, vv in v.items()} for k, v in table.items()},
         "gpu_launches": launches,
         "clocks": clk,
