@@ -195,6 +195,38 @@ int gdsw_gmres(const gdsw_csr* a, gdsw_precond* m, const gdsw_csr* m_csr, const 
                gdsw_solve_report* rep, double* history, int32_t* true_it, double* true_res,
                int32_t cap, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Sharded solve: one process per GPU, each rank owns a
+ * contiguous row range [own_lo, own_hi) of its extended local layout of
+ * n_ext rows (owned rows + halo rows owned by neighbours) and a contiguous
+ * range of subdomains. Collectives are this library's own peer-memory
+ * kernels: every rank maps every rank's IPC-exported mailbox (exchange the
+ * 64-byte handles with any bootstrap, e.g. torch.distributed); one kernel
+ * per collective, device-side release/acquire flags, no host round trip.
+ * Per GMRES iteration: one halo refresh before the SpMV and one before the
+ * apply, one reverse halo of overlapped partial sums, one all-reduce of the
+ * coarse right-hand side and ONE all-reduce of the fused block.
+ * send ranges: owned rows neighbour i needs; recv ranges: halo rows it owns
+ * (both ext-local). The operator passed to gdsw_gmres_dist has n_own rows
+ * and n_ext columns; the preconditioner's plan is built on n_ext rows.
+ * ---------------------------------------------------------------------- */
+typedef struct gdsw_dist gdsw_dist;
+int gdsw_dist_create(gdsw_dist** out, int rank, int nranks, int64_t n_ext, int64_t own_lo,
+                     int64_t own_hi, int n_nbr, const int32_t* nbr_rank, const int64_t* send_lo,
+                     const int64_t* send_hi, const int64_t* recv_lo, const int64_t* recv_hi,
+                     int64_t red_max);
+int gdsw_dist_ipc_handle(gdsw_dist* d, void* handle64);
+int gdsw_dist_open_peers(gdsw_dist* d, const void* handles /* nranks x 64 bytes */);
+int gdsw_dist_allreduce(gdsw_dist* d, const double* in, double* out, int64_t m, void* stream);
+int gdsw_dist_halo(gdsw_dist* d, double* x_ext, void* stream);
+int gdsw_dist_destroy(gdsw_dist* d);
+int gdsw_precond_set_dist(gdsw_precond* m, gdsw_dist* d);
+/* b, x: owned rows only (n_own) */
+int gdsw_gmres_dist(const gdsw_csr* a, gdsw_precond* m, const gdsw_csr* m_csr, const double* b,
+                    double* x, int x0_nonzero, const gdsw_krylov_cfg* cfg, gdsw_workspace* ws,
+                    gdsw_dist* dist, gdsw_solve_report* rep, double* history, int32_t* true_it,
+                    double* true_res, int32_t cap, void* stream);
+
 /* fused single-reduce block reduction [V[:j]; v]^T [v, z] (krylov.py:290-300);
  * out (host) receives 2(j+1) values: [V.v..., v.v, V.z..., v.z] */
 int gdsw_block_dot(const double* V, int64_t ldv, int32_t j, const double* v, const double* z,

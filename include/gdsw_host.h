@@ -50,6 +50,9 @@ int gh_node_graph(int64_t n_nodes, int64_t dpn, const int64_t* a_ptr,
                   const int64_t* a_idx, gh_result** out);      /* {ptr, idx} */
 int gh_expand_layers(int64_t n, const int64_t* g_ptr, const int64_t* g_idx,
                      uint8_t* mask, int64_t layers);
+int gh_overlap_sets(int64_t n_nodes, const int64_t* g_ptr, const int64_t* g_idx,
+                    const int64_t* node_owner, int64_t n_parts, int64_t n_subs,
+                    const int64_t* subs, int64_t layers, gh_result** out); /* {ptr, nodes} */
 int gh_nested_dissection(int64_t n, const int64_t* a_ptr, const int64_t* a_idx,
                          int64_t leaf_size, int64_t* perm_out);
 int gh_symbolic_lu(int64_t n, const int64_t* a_ptr, const int64_t* a_idx,

@@ -182,3 +182,11 @@ def spmv(ptr, idx, val, x, y, alpha, beta):
         _check(_lib.gh_spmv_f32(C.c_int64(ptr.size - 1), _p(ptr), _p(idx), _p(val), _p(x),
                                 _p(y), C.c_float(alpha), C.c_float(beta)))
     return y
+
+
+def overlap_sets(g_ptr, g_idx, node_owner, n_parts: int, subs, layers: int):
+    g_ptr, g_idx, node_owner, subs = _i64(g_ptr), _i64(g_idx), _i64(node_owner), _i64(subs)
+    ptr, nodes = _call(_lib.gh_overlap_sets, C.c_int64(node_owner.size), _p(g_ptr), _p(g_idx),
+                       _p(node_owner), C.c_int64(n_parts), C.c_int64(subs.size), _p(subs),
+                       C.c_int64(layers))
+    return [nodes[ptr[k]:ptr[k + 1]] for k in range(subs.size)]

@@ -69,6 +69,62 @@ __global__ void k_restrict_final(RestrictDev R, const T* __restrict__ pgt_val,
 }
 
 // ---------------------------------------------------------------------------
+// partial sums received from other ranks (sharded solve). Rows owned by this
+// rank that lower-ranked (= lower subdomain ids) ranks overlap start their
+// ordered accumulation from the lower partial; rows overlapped by higher
+// ranks add the higher partial after the own contributions -- the single-GPU
+// order `z[dofs_i] += y_i` for ascending i. Empty ranges on one GPU.
+// ---------------------------------------------------------------------------
+struct RemoteAdd {
+  const double* recv = nullptr;
+  int64_t pre_lo = 0, pre_hi = 0, post_lo = 0, post_hi = 0;
+  template <typename T>
+  __device__ __forceinline__ T start(int64_t g) const {
+    return (g >= pre_lo && g < pre_hi) ? (T)recv[g] : T(0);
+  }
+  template <typename T>
+  __device__ __forceinline__ T finish(int64_t g, T acc) const {
+    return (g >= post_lo && g < post_hi) ? rn_add(acc, (T)recv[g]) : acc;
+  }
+};
+
+template <typename T>
+__global__ void k_cast_to_f64(int64_t n, const T* __restrict__ a, double* __restrict__ b) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = (double)a[i];
+}
+template <typename T>
+__global__ void k_cast_from_f64(int64_t n, const double* __restrict__ a, T* __restrict__ b) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = (T)a[i];
+}
+
+// one-level scatter over owned rows [lo, hi): z[g] = double(sum of y in
+// ascending subdomain order), remote partials folded in order
+template <typename T>
+__global__ void k_scatter_owned(int64_t lo, int64_t hi, const int32_t* __restrict__ sc_ptr,
+                                const int32_t* __restrict__ sc_pos, const T* __restrict__ y,
+                                RemoteAdd RA, double* __restrict__ z) {
+  const int64_t g = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= hi) return;
+  T acc = RA.start<T>(g);
+  for (int32_t q = sc_ptr[g]; q < sc_ptr[g + 1]; ++q) acc = rn_add(acc, y[sc_pos[q]]);
+  z[g] = (double)RA.finish<T>(g, acc);
+}
+
+// this rank's contributions to rows owned by other ranks (its halo rows)
+template <typename T>
+__global__ void k_scatter_partial(int64_t lo, int64_t hi, const int32_t* __restrict__ sc_ptr,
+                                  const int32_t* __restrict__ sc_pos, const T* __restrict__ y,
+                                  double* __restrict__ part) {
+  const int64_t g = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= hi) return;
+  T acc = T(0);
+  for (int32_t q = sc_ptr[g]; q < sc_ptr[g + 1]; ++q) acc = rn_add(acc, y[sc_pos[q]]);
+  part[g] = (double)acc;
+}
+
+// ---------------------------------------------------------------------------
 // chunked restriction / prolongation (chunks of <= 256 interior rows that
 // never straddle a subdomain, shared with the extension solver)
 // ---------------------------------------------------------------------------
@@ -153,6 +209,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_prolong_interior(ChunkDev D, con
                                                                  const int32_t* __restrict__ sc_ptr,
                                                                  const int32_t* __restrict__ sc_pos,
                                                                  const T* __restrict__ y,
+                                                                 RemoteAdd RA,
                                                                  double* __restrict__ z) {
   const int32_t ch = blockIdx.x;
   if (threadIdx.x >= D.chunk_nrow[ch]) return;
@@ -164,9 +221,9 @@ __global__ void __launch_bounds__(CH_THREADS) k_prolong_interior(ChunkDev D, con
   T zc = T(0);
   for (int32_t c = D.col_ptr[s]; c < D.col_ptr[s + 1]; ++c, pr += ni)
     zc = rn_add(zc, rn_mul(ldg_stream(pr), v[D.col_ids[c]]));
-  T acc = T(0);
+  T acc = RA.start<T>(g);
   for (int32_t q = sc_ptr[g]; q < sc_ptr[g + 1]; ++q) acc = rn_add(acc, y[sc_pos[q]]);
-  z[g] = (double)rn_add(zc, acc);
+  z[g] = (double)rn_add(zc, RA.finish<T>(g, acc));
 }
 
 // interface rows: Phi_Gamma row (CSR by interface position) + scatter
@@ -179,15 +236,16 @@ __global__ void __launch_bounds__(256) k_prolong_interface(int32_t n_gamma, cons
                                                            const int32_t* __restrict__ sc_ptr,
                                                            const int32_t* __restrict__ sc_pos,
                                                            const T* __restrict__ y,
+                                                           RemoteAdd RA,
                                                            double* __restrict__ z) {
   const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n_gamma) return;
   const int32_t g = gamma_rows[t];
   T zc = T(0);
   for (int64_t p = pg_ptr[t]; p < pg_ptr[t + 1]; ++p) zc = rn_add(zc, rn_mul(pg_val[p], v[pg_col[p]]));
-  T acc = T(0);
+  T acc = RA.start<T>(g);
   for (int32_t q = sc_ptr[g]; q < sc_ptr[g + 1]; ++q) acc = rn_add(acc, y[sc_pos[q]]);
-  z[g] = (double)rn_add(zc, acc);
+  z[g] = (double)rn_add(zc, RA.finish<T>(g, acc));
 }
 
 // dense replicated coarse solve: v = A0^-1 u, one warp per row

@@ -13,6 +13,7 @@
 #include "../../include/gdsw.h"
 #include "coarse.cuh"
 #include "common.cuh"
+#include "dist.cuh"
 #include "extension.cuh"
 #include "fastilu.cuh"
 #include "krylov.cuh"
@@ -538,6 +539,9 @@ extern "C" int gdsw_plan_destroy(gdsw_plan* p) {
 struct gdsw_precond {
   gdsw_plan* plan = nullptr;
   std::unique_ptr<CoarsePlan> cp;
+  gdsw_dist* dist = nullptr;         // sharded layout (not owned)
+  DBuf<double> part_ext, recv_ext;   // reverse-halo partial sums (ext-local)
+  DBuf<double> red64;                // coarse rhs reduction scratch
   int dtype = GDSW_F64;
   size_t es = 8;
   int iters = 5;
@@ -700,6 +704,12 @@ template <typename T>
 void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
   gdsw_plan* P = m->plan;
   CoarsePlan* Cp = m->cp.get();
+  gdsw_dist* Dd = m->dist;
+  if (Dd) {
+    // halo rows of the (extended) input from their owners
+    ProfScope ps("halo_fwd", s, 0.0);
+    Dd->halo_fwd(const_cast<double*>(r), s);
+  }
   if (Cp) {
     ChunkDev D = Cp->chunk_dev();
     if (Cp->n_chunks > 0) {
@@ -716,12 +726,40 @@ void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
                                                     Cp->cpart_idx.p, (const T*)m->pdot.p, (T*)m->cu.p);
       CK_LAUNCH();
     }
+    if (Dd) {
+      // coarse right-hand side: every rank's partial, summed in rank order
+      ProfScope ps("coarse_allreduce", s, 0.0);
+      k_cast_to_f64<T><<<grid_for(Cp->n_c, TB), TB, 0, s>>>(Cp->n_c, (const T*)m->cu.p, m->red64.p);
+      CK_LAUNCH();
+      Dd->allreduce(m->red64.p, m->red64.p + Cp->n_c, Cp->n_c, s);
+      k_cast_from_f64<T><<<grid_for(Cp->n_c, TB), TB, 0, s>>>(Cp->n_c, m->red64.p + Cp->n_c, (T*)m->cu.p);
+      CK_LAUNCH();
+    }
     ProfScope ps("coarse_solve", s, (double)Cp->n_c * Cp->n_c * sizeof(T));
     k_coarse_gemv<T><<<grid_for(Cp->n_c, TB / 32), TB, 0, s>>>(Cp->n_c, (const T*)m->ainv.p,
                                                                (const T*)m->cu.p, (T*)m->cv.p);
     CK_LAUNCH();
   }
   T* y = local_solve<T>(m, r, 0, s);
+  RemoteAdd RA{};
+  int64_t own_lo = 0, own_hi = P->n;
+  if (Dd) {
+    // my subdomains' contributions to rows other ranks own, sent to them;
+    // theirs to my rows received, combined in subdomain order below
+    ProfScope ps("halo_rev", s, 0.0);
+    for (int i = 0; i < Dd->halo.nn; ++i) {
+      const int64_t lo = Dd->halo.recv_lo[i], hi = Dd->halo.recv_hi[i];
+      if (hi > lo) {
+        k_scatter_partial<T><<<grid_for(hi - lo, TB), TB, 0, s>>>(lo, hi, P->sc_ptr.p, P->sc_pos.p, y,
+                                                                  m->part_ext.p);
+        CK_LAUNCH();
+      }
+    }
+    Dd->halo_rev(m->part_ext.p, m->recv_ext.p, s);
+    RA = RemoteAdd{m->recv_ext.p, Dd->pre_lo, Dd->pre_hi, Dd->post_lo, Dd->post_hi};
+    own_lo = Dd->own_off;
+    own_hi = Dd->own_off + Dd->n_own;
+  }
   if (Cp) {
     ChunkDev D = Cp->chunk_dev();
     // interior rows: panel row dot (coalesced) + their local contributions
@@ -729,7 +767,7 @@ void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
       ProfScope ps("prolong_interior", s, (double)Cp->panel_entries * sizeof(T) +
                                               Cp->n_int_total * (4.0 + 8.0 + 8.0 + 4.0 + sizeof(T)));
       k_prolong_interior<T><<<Cp->n_chunks, CH_THREADS, 0, s>>>(D, (const T*)m->panel(), (const T*)m->cv.p,
-                                                               P->sc_ptr.p, P->sc_pos.p, y, z);
+                                                               P->sc_ptr.p, P->sc_pos.p, y, RA, z);
       CK_LAUNCH();
     }
     const double ng = (double)Cp->n_gamma;
@@ -739,14 +777,13 @@ void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
     if (Cp->n_gamma > 0) {
       k_prolong_interface<T><<<grid_for(Cp->n_gamma, TB), TB, 0, s>>>(
           (int32_t)Cp->n_gamma, Cp->gamma32.p, Cp->pgam_ptr.p, Cp->pgam_col.p, (const T*)m->pgr_val.p,
-          (const T*)m->cv.p, P->sc_ptr.p, P->sc_pos.p, y, z);
+          (const T*)m->cv.p, P->sc_ptr.p, P->sc_pos.p, y, RA, z);
       CK_LAUNCH();
     }
   } else {
     ProfScope ps("scatter", s, P->n_loc * (4.0 + sizeof(T)) + (P->n + 1) * 4.0 + P->n * 8.0);
-    k_scatter_prolong<T><<<grid_for(P->n, TB), TB, 0, s>>>(
-        (int32_t)P->n, P->sc_ptr.p, P->sc_pos.p, y, ProlongDev{}, (const T*)nullptr, (const T*)nullptr,
-        (const T*)nullptr, z);
+    k_scatter_owned<T><<<grid_for(own_hi - own_lo, TB), TB, 0, s>>>(own_lo, own_hi, P->sc_ptr.p,
+                                                                    P->sc_pos.p, y, RA, z);
     CK_LAUNCH();
   }
 }
@@ -809,6 +846,7 @@ int gdsw_precond_set_coarse(gdsw_precond* m, const gdsw_coarse_desc* desc) {
     m->cv.alloc(std::max<int32_t>(cp->n_c, 1) * m->es);
     m->panel64.alloc(std::max<int64_t>(cp->panel_entries, 1));
     if (m->dtype == GDSW_F32) m->panel32.alloc(std::max<int64_t>(cp->panel_entries, 1) * 4);
+    m->red64.alloc(2 * (size_t)std::max(cp->n_c, 1));
     CK(cudaDeviceSynchronize());
     m->cp = std::move(cp);
     m->has_phi = m->has_ainv = false;

@@ -379,6 +379,51 @@ int gh_expand_layers(int64_t n, const int64_t* g_ptr, const int64_t* g_idx,
   })
 }
 
+// overlap node sets of the listed subdomains: seeds = nodes owned by s,
+// grown by `layers` graph layers (same sets as extend_overlap,
+// decomposition.py:150-166), without a full-size mask per subdomain
+int gh_overlap_sets(int64_t n_nodes, const int64_t* g_ptr, const int64_t* g_idx,
+                    const int64_t* node_owner, int64_t n_parts, int64_t n_subs,
+                    const int64_t* subs, int64_t layers, gh_result** out) {
+  GH_TRY({
+    VI cnt(n_parts + 1, 0);
+    for (i64 u = 0; u < n_nodes; ++u) cnt[node_owner[u] + 1]++;
+    for (i64 s = 0; s < n_parts; ++s) cnt[s + 1] += cnt[s];
+    VI byown(n_nodes), off(cnt.begin(), cnt.end() - 1);
+    for (i64 u = 0; u < n_nodes; ++u) byown[off[node_owner[u]]++] = u;
+    VI stamp(n_nodes, -1), ptr(1, 0), nodes, frontier, nxt;
+    for (i64 t = 0; t < n_subs; ++t) {
+      const i64 s = subs[t];
+      const i64 start = (i64)nodes.size();
+      frontier.assign(byown.begin() + cnt[s], byown.begin() + cnt[s + 1]);
+      for (i64 u : frontier) {
+        stamp[u] = t;
+        nodes.push_back(u);
+      }
+      for (i64 l = 0; l < layers; ++l) {
+        nxt.clear();
+        for (i64 v : frontier)
+          for (i64 p = g_ptr[v]; p < g_ptr[v + 1]; ++p) {
+            i64 w = g_idx[p];
+            if (stamp[w] != t) {
+              stamp[w] = t;
+              nxt.push_back(w);
+              nodes.push_back(w);
+            }
+          }
+        frontier.swap(nxt);
+        if (frontier.empty()) break;
+      }
+      std::sort(nodes.begin() + start, nodes.end());
+      ptr.push_back((i64)nodes.size());
+    }
+    auto* r = new gh_result;
+    r->add(std::move(ptr));
+    r->add(std::move(nodes));
+    *out = r;
+  })
+}
+
 int gh_nested_dissection(int64_t n, const int64_t* a_ptr, const int64_t* a_idx,
                          int64_t leaf_size, int64_t* perm_out) {
   GH_TRY({

@@ -79,6 +79,18 @@ _SIGS = {
                              C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "gdsw_block_dot": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
                                  C.c_int64, C.c_void_p, C.c_void_p]),
+    "gdsw_dist_create": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                                   C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_int64]),
+    "gdsw_dist_ipc_handle": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gdsw_dist_open_peers": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gdsw_dist_allreduce": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    "gdsw_dist_halo": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gdsw_dist_destroy": (C.c_int, [C.c_void_p]),
+    "gdsw_precond_set_dist": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gdsw_gmres_dist": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "gdsw_launch_count": (C.c_int64, []),
     "gdsw_prof_enable": (C.c_int, [C.c_int]),
     "gdsw_prof_reset": (C.c_int, []),
@@ -352,6 +364,75 @@ def gmres_device(a_dev: DeviceCsr, m_pre: Precond | None, m_csr: DeviceCsr | Non
                         m_csr.handle if m_csr else None, _ptr(b), _ptr(x),
                         1 if x0_nonzero else 0, C.byref(kc), ws.handle, C.byref(rep),
                         _ptr(hist), _ptr(tit), _ptr(tres), cap, stream_handle()))
+    return dict(iterations=rep.iterations, converged=bool(rep.converged),
+                reduction_count=rep.reduction_count,
+                iteration_reductions=rep.iteration_reductions,
+                residual_reductions=rep.residual_reductions, restarts=rep.restarts,
+                history=hist[:rep.n_history].copy(),
+                true_residuals=[(int(tit[k]), float(tres[k])) for k in range(rep.n_true)])
+
+
+class DistLayout:
+    """gdsw_dist: this rank's extended layout + peer-memory mailbox."""
+
+    def __init__(self, rank, nranks, n_ext, own_lo, own_hi, nbrs, red_max=4096):
+        nb = len(nbrs)
+        ranks = np.array([q for q, *_ in nbrs] or [0], dtype=np.int32)
+        cols = [np.array([t[k] for t in nbrs] or [0], dtype=np.int64) for k in range(1, 5)]
+        h = C.c_void_p()
+        _ck(_lib.gdsw_dist_create(C.byref(h), int(rank), int(nranks), int(n_ext), int(own_lo),
+                                  int(own_hi), nb, _ptr(ranks), *[_ptr(c) for c in cols],
+                                  int(red_max)))
+        self.handle = h
+        self.rank, self.nranks = rank, nranks
+        self.n_ext, self.own_lo, self.own_hi = n_ext, own_lo, own_hi
+
+    def ipc_handle(self) -> bytes:
+        buf = (C.c_char * 64)()
+        _ck(_lib.gdsw_dist_ipc_handle(self.handle, C.cast(buf, C.c_void_p)))
+        return bytes(buf)
+
+    def open_peers(self, handles: list):
+        blob = b"".join(handles)
+        buf = (C.c_char * len(blob)).from_buffer_copy(blob)
+        _ck(_lib.gdsw_dist_open_peers(self.handle, C.cast(buf, C.c_void_p)))
+
+    def allreduce(self, x_in, x_out):
+        _ck(_lib.gdsw_dist_allreduce(self.handle, _ptr(x_in), _ptr(x_out), int(x_in.numel()),
+                                     stream_handle()))
+        return x_out
+
+    def halo(self, x_ext):
+        _ck(_lib.gdsw_dist_halo(self.handle, _ptr(x_ext), stream_handle()))
+        return x_ext
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and _lib is not None:
+            _lib.gdsw_dist_destroy(h)
+            self.handle = None
+
+
+def precond_set_dist(pre: "Precond", layout: DistLayout | None):
+    _ck(_lib.gdsw_precond_set_dist(pre.handle, layout.handle if layout else None))
+
+
+def gmres_dist(a_own: DeviceCsr, m_pre, b_own, x_own, x0_nonzero: bool, cfg,
+               layout: DistLayout) -> dict:
+    """Sharded native GMRES: b_own/x_own are this rank's owned rows."""
+    ws = workspace(layout.n_ext, cfg.restart)
+    kc = _KrylovCfg(cfg.restart, cfg.rel_tol, cfg.max_iters,
+                    1 if cfg.variant == "single_reduce" else 0,
+                    1 if cfg.orthogonalization == "cgs2" else 0)
+    rep = _Report()
+    cap = 2 * cfg.max_iters + 8
+    hist = np.zeros(cap, dtype=np.float64)
+    tit = np.zeros(cap, dtype=np.int32)
+    tres = np.zeros(cap, dtype=np.float64)
+    _ck(_lib.gdsw_gmres_dist(a_own.handle, m_pre.handle if m_pre else None, None, _ptr(b_own),
+                             _ptr(x_own), 1 if x0_nonzero else 0, C.byref(kc), ws.handle,
+                             layout.handle, C.byref(rep), _ptr(hist), _ptr(tit), _ptr(tres), cap,
+                             stream_handle()))
     return dict(iterations=rep.iterations, converged=bool(rep.converged),
                 reduction_count=rep.reduction_count,
                 iteration_reductions=rep.iteration_reductions,
