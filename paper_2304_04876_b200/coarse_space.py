@@ -129,11 +129,13 @@ def _row_entries(ptr: np.ndarray, rows: np.ndarray) -> np.ndarray:
 
 
 def coarse_desc(a: CsrMatrix, structure: InterfaceStructure, pg: CsrMatrix, n_cols: int,
-                sets: list) -> dict:
+                sets: list, gamma: np.ndarray | None = None) -> dict:
     """Device descriptor of the coarse structure: interface rows of Phi,
     per-subdomain interior rows and touching coarse columns, and the A_II /
-    A_IG patterns with their A.values positions."""
-    gamma = structure.interface
+    A_IG patterns with their A.values positions. `gamma` overrides the
+    interface row list (a rank's owned interface rows, sharded solve)."""
+    if gamma is None:
+        gamma = structure.interface
     int_ptr = np.zeros(len(sets) + 1, dtype=np.int64)
     col_lists, aii, aig = [], [], []
     for s, dofs in enumerate(sets):
