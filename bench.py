@@ -21,8 +21,10 @@ FastSpTRSV(5 iterates) local solves, natural ordering, fp64.
 
 --impl reference: the reference's CPU path (the oracle port, entirely on the
 host, its own exact-LU coarse basis) on the same workload, bounded samples.
-Multi-GPU (torchrun): each rank solves its own 2M-dof C2 system (replicas;
-the sharded single-system solve is the next row of the build).
+Multi-GPU (torchrun, weak scaling): ONE global system of N x 2M dof
+(128 x 128 x 128N grid, 4 x 4 x 4N boxes) sharded in z-slabs, 64 subdomains
+per GPU; halos, the coarse right-hand side and the GMRES block go through
+libgdsw's peer-memory collectives (paper_2304_04876_b200.dist).
 """
 
 from __future__ import annotations
@@ -35,6 +37,7 @@ import subprocess
 import sys
 import tempfile
 import time
+import types
 from pathlib import Path
 
 import numpy as np
@@ -56,8 +59,11 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="native", choices=("native", "reference"))
-    p.add_argument("--n", type=int, default=128, help="grid nodes per axis (per GPU)")
-    p.add_argument("--parts", type=int, default=4, help="subdomain boxes per axis (per GPU)")
+    # (not --n / --parts: torchrun's parser would claim those prefixes)
+    p.add_argument("--grid", dest="n", type=int, default=128,
+                   help="grid nodes per axis (per GPU)")
+    p.add_argument("--boxes", dest="parts", type=int, default=4,
+                   help="subdomain boxes per axis (per GPU)")
     p.add_argument("--solver", default="fast_ilu(0,3,5)")
     p.add_argument("--ordering", default="natural")
     p.add_argument("--precision", default="double")
@@ -82,27 +88,37 @@ def solver_spec(token: str):
     return SolverSpec("fast_ilu", fill, sweeps, iters)
 
 
+def build_problem_config(args):
+    from paper_2304_04876_b200.schwarz import SchwarzConfig
+    return SchwarzConfig(local=solver_spec(args.solver), ordering=args.ordering,
+                         precision=args.precision)
+
+
 def build_problem(args):
     from paper_2304_04876_b200.decomposition import box_partition, decompose
     from paper_2304_04876_b200.model_problems import Grid3D, assemble_laplace3d
-    from paper_2304_04876_b200.schwarz import SchwarzConfig
     prob = assemble_laplace3d(Grid3D(args.n, args.n, args.n))
     part = box_partition(prob.grid, args.parts, args.parts, args.parts)
     dec = decompose(prob.a, part, 1, "rgdsw")
-    cfg = SchwarzConfig(local=solver_spec(args.solver), ordering=args.ordering,
-                        precision=args.precision)
-    return prob, dec, cfg
+    return prob, dec, build_problem_config(args)
 
 
-def workload(args) -> dict:
+def workload(args, world: int = 1) -> dict:
     n = args.n ** 3
+    if world > 1:
+        par = (f"sharded x{world}: z-slabs of {args.parts ** 3} subdomains per GPU, global "
+               f"{args.n}x{args.n}x{args.n * world} grid / {args.parts}x{args.parts}x"
+               f"{args.parts * world} boxes; halos, coarse rhs and the GMRES block over "
+               "libgdsw peer-memory collectives (CUDA IPC, NVLink)")
+    else:
+        par = "single GPU"
     return {"workload": (f"C2: 3D Laplace 7-pt {args.n}^3 ({n:,} dof per GPU), "
                          f"{args.parts}x{args.parts}x{args.parts}={args.parts ** 3} subdomains "
                          f"per GPU, overlap 1, rGDSW, {args.solver} local solves, "
                          f"{args.ordering} ordering, {args.precision} preconditioner, "
                          "single-reduce GMRES(30) to rtol 1e-7, x0=0"),
             "dof_per_gpu": n, "subdomains_per_gpu": args.parts ** 3,
-            "parallelism": f"replicas x{args.gpus} (one independent C2 system per GPU)",
+            "parallelism": par,
             "l2": "no flush: per-solve working set (A, factors, Phi panels, 2x30 Krylov "
                   "vectors ~1.9 GB) >> 126 MB L2"}
 
@@ -188,9 +204,15 @@ def native(args):
     from paper_2304_04876_b200.schwarz import setup_numeric, setup_symbolic
 
     world, rank, local = dist_setup()
+    # GDSW_SAME_DEVICE=1: every rank on cuda:0 (functional check of the
+    # sharded path on a single-GPU box; timings are then meaningless)
+    if os.environ.get("GDSW_SAME_DEVICE") == "1":
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # bootstrap only (IPC handles, dense A0 partials, timing max); the data
+        # path uses libgdsw's own peer-memory collectives
+        tdist.init_process_group("gloo")
 
     def barrier():
         if world > 1:
@@ -199,28 +221,51 @@ def native(args):
     def max_over_ranks(v: float) -> float:
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        t = torch.tensor([v], dtype=torch.float64)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         return float(t.item())
 
+    kcfg = KrylovConfig(variant="single_reduce")
     t0 = time.perf_counter()
-    prob, dec, cfg = build_problem(args)
+    if world == 1:
+        prob, dec, cfg = build_problem(args)
+    else:
+        from paper_2304_04876_b200.dist import build_sharded_problem
+        prob, dec = build_sharded_problem(args.n, args.n, args.parts, args.parts, world)
+        cfg = build_problem_config(args)
     t_inputs = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    skel = setup_symbolic(prob.a, dec, cfg)
-    t_sym = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    pre = setup_numeric(skel, prob.a, prob.nullspace)
-    torch.cuda.synchronize()
-    t_num = time.perf_counter() - t0
     n = prob.a.nrows
     x_star = np.random.default_rng(0).standard_normal(n)
     b = prob.a @ x_star
-    b_dev = torch.from_numpy(b).cuda()
-    kcfg = KrylovConfig(variant="single_reduce")
+    t0 = time.perf_counter()
+    if world == 1:
+        skel = setup_symbolic(prob.a, dec, cfg)
+        t_sym = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        pre = setup_numeric(skel, prob.a, prob.nullspace)
+        g0, g1 = 0, n
+
+        def solve(bd):
+            return gmres(prob.a, pre, bd, kcfg)
+    else:
+        from paper_2304_04876_b200.dist import DistPreconditioner, plan_shards
+        sh = plan_shards(prob.a, dec, world)[rank]
+        t_sym = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        dpre = DistPreconditioner(prob.a, dec, cfg, prob.nullspace, sh)
+        g0, g1 = sh.g0, sh.g1
+
+        def solve(bd):
+            bd = bd if bd.is_cuda else bd.to("cuda", non_blocking=True)
+            x, out = dpre.solve(bd, kcfg)
+            return x, types.SimpleNamespace(iterations=out["iterations"],
+                                            converged=out["converged"])
+    torch.cuda.synchronize()
+    t_num = time.perf_counter() - t0
+    b_dev = torch.from_numpy(b[g0:g1].copy()).cuda()
 
     for _ in range(args.warmup):
-        x, rep = gmres(prob.a, pre, b_dev, kcfg)
+        x, rep = solve(b_dev)
     torch.cuda.synchronize()
 
     stream = torch.cuda.current_stream()
@@ -234,7 +279,7 @@ def native(args):
     e0.record(stream)
     reps = []
     for _ in range(args.steps):
-        x, rep = gmres(prob.a, pre, b_dev, kcfg)
+        x, rep = solve(b_dev)
         reps.append(rep)
     e1.record(stream)
     torch.cuda.synchronize()
@@ -250,12 +295,16 @@ def native(args):
     device.prof_reset()
     device.prof_enable(True)
     for _ in range(args.steps):
-        gmres(prob.a, pre, b_dev, kcfg)
+        solve(b_dev)
     torch.cuda.synchronize()
     device.prof_enable(False)
     phases = device.prof_read()
     its = reps[-1].iterations
     xh = x.cpu().numpy()
+    if world > 1:
+        pieces = [None] * world
+        tdist.all_gather_object(pieces, xh)
+        xh = np.concatenate(pieces)
     true_res = float(np.linalg.norm(b - prob.a @ xh) / np.linalg.norm(b))
     true_err = float(np.linalg.norm(xh - x_star) / np.linalg.norm(x_star))
 
@@ -269,7 +318,8 @@ def native(args):
                            us_per_launch=1e3 * ph["ms"] / ph["launches"],
                            bytes_per_launch=ph["bytes"] / ph["launches"],
                            gbs=ph["bytes"] / (ph["ms"] * 1e-3) / 1e9)
-    dom = max(table, key=lambda k: table[k]["ms_total"])
+    dom = max((k for k in table if table[k]["bytes_per_launch"] > 0),
+              key=lambda k: table[k]["ms_total"])
     d = table[dom]
     app_ms = sum(table[k]["ms_total"] for k in APPLY_PHASES if k in table)
     app_bytes = sum(phases[k]["bytes"] for k in APPLY_PHASES if k in table)
@@ -277,19 +327,22 @@ def native(args):
     apply_gbs = app_bytes / (app_ms * 1e-3) / 1e9 if app_ms else None
     solve_ms = e0.elapsed_time(e1) / args.steps
     step_bytes = sum(ph["bytes"] for ph in phases.values()) / args.steps
+    comm_ms = sum(table[k]["ms_total"] for k in ("halo_fwd", "halo_rev", "block_allreduce",
+                                                 "coarse_allreduce") if k in table) / args.steps
     result = {
         "metric": METRIC, "value": ms_step / 1e3, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference generators (assemble_laplace3d), x*=default_rng(0)."
                 "standard_normal(n), b=A x*",
-        "config": workload(args),
+        "config": workload(args, world),
         "iterations": its, "converged": bool(reps[-1].converged),
         "ms_per_iteration": ms_step / max(its, 1),
         "true_rel_residual": true_res, "true_error": true_err,
         "apply_gbs": apply_gbs, "apply_frac_of_hbm": apply_gbs / peak if apply_gbs else None,
         "apply_ms": app_ms / n_apply,
         "solve_gbs": step_bytes / (solve_ms * 1e-3) / 1e9,
+        "comm_ms_per_solve": comm_ms,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": d["gbs"], "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": d["gbs"] / peak,
                      "traffic": (ncu_traffic(dom) or {}).get("bytes"),
@@ -304,22 +357,32 @@ def native(args):
         "setup_s": {"inputs": t_inputs, "symbolic_host": t_sym, "numeric": t_num},
     }
     if not args.no_e2e:
-        bh = torch.from_numpy(b).pin_memory()
-        for _ in range(1):
-            gmres(prob.a, pre, bh, kcfg)
+        bh = torch.from_numpy(b[g0:g1].copy()).pin_memory()
+        if world == 1:
+            def solve_host(bh):
+                return gmres(prob.a, pre, bh, kcfg)
+        else:
+            def solve_host(bh):
+                x, r = solve(bh.to("cuda", non_blocking=True))
+                return x.cpu(), r
+        solve_host(bh)
         torch.cuda.synchronize()
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         for _ in range(args.e2e_steps):
-            xe, repe = gmres(prob.a, pre, bh, kcfg)
+            xe, repe = solve_host(bh)
         f1.record(stream)
         torch.cuda.synchronize()
         barrier()
         e2e_ms = max_over_ranks(f0.elapsed_time(f1) / args.e2e_steps)
-        result["e2e"] = {"value": e2e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": n * 8,
-                         "d2h_bytes_per_step": n * 8 + 8 * 2 * 31 * repe.iterations,
-                         "api": "paper_2304_04876_b200.krylov.gmres(A, M, pinned host b)"}
+        nb = (g1 - g0) * 8
+        result["e2e"] = {"value": e2e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": nb * world,
+                         "d2h_bytes_per_step": (nb + 8 * 2 * 31 * repe.iterations) * world,
+                         "api": ("paper_2304_04876_b200.krylov.gmres(A, M, pinned host b)"
+                                 if world == 1 else
+                                 "paper_2304_04876_b200.dist.DistPreconditioner.solve "
+                                 "(pinned host b -> device, x -> host)")}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(args, prob, dec, cfg, skel, pre, b, its)
     if world > 1:
