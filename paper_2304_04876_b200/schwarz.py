@@ -86,6 +86,19 @@ def _pattern_fingerprint(a: CsrMatrix) -> str:
 # device plan assembly (batched-subdomain layout)
 # ---------------------------------------------------------------------------
 
+def host_map(fn, items) -> list:
+    """Per-subdomain host setup work on all cores (the native symbolic and
+    numeric kernels release the GIL); results in input order."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    items = list(items)
+    workers = min(len(items), os.cpu_count() or 1)
+    if workers <= 1:
+        return [fn(x) for x in items]
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        return list(ex.map(fn, items))
+
+
 def _cat(arrays, dtype=np.int64):
     return np.concatenate(arrays).astype(dtype, copy=False) if arrays else np.zeros(0, dtype)
 
@@ -320,11 +333,11 @@ def setup_symbolic(a: CsrMatrix, decomp: Decomposition,
     sets = [np.asarray(s, dtype=np.int64) for s in decomp.overlap.sets]
     if sum(s.size for s in sets) < n:
         raise ValueError("overlap sets do not cover the operator")
-    local_symbolics = []
-    for dofs in sets:
+    def one(dofs):
         block = extract_submatrix(a, dofs, dofs)
-        local_symbolics.append(build_symbolic(block, config.local,
-                                              make_ordering(block, config.ordering)))
+        return build_symbolic(block, config.local, make_ordering(block, config.ordering))
+
+    local_symbolics = host_map(one, sets)
     isets = _interior_sets(part, structure) if config.use_coarse else []
     pattern = CsrMatrix(a.nrows, a.ncols, a.row_ptr, a.col_idx,
                         np.zeros(a.nnz, dtype=np.float64))
@@ -393,13 +406,20 @@ def setup_numeric(skeleton: PreconditionerSkeleton, a: CsrMatrix,
     else:
         lvs, uvs, facs = [], [], []
         shift = spec.diag_shift if spec.method == "ilu_k" else 0.0
-        for i, (dofs, sym) in enumerate(zip(skeleton.sets, skeleton.local_symbolics)):
-            block = extract_submatrix(local_src, dofs, dofs)
+
+        def one(item):
+            dofs, sym = item
             try:
-                lv, uv = host_numeric(block, sym, shift)
+                return host_numeric(extract_submatrix(local_src, dofs, dofs), sym, shift)
             except np.linalg.LinAlgError as err:
+                return err
+
+        results = host_map(one, list(zip(skeleton.sets, skeleton.local_symbolics)))
+        for i, (res, sym) in enumerate(zip(results, skeleton.local_symbolics)):
+            if isinstance(res, Exception):   # first failing subdomain, in order
                 raise np.linalg.LinAlgError(
-                    f"local matrix of subdomain {i} failed to factor: {err}") from err
+                    f"local matrix of subdomain {i} failed to factor: {res}") from res
+            lv, uv = res
             lvs.append(lv)
             uvs.append(uv)
             facs.append(LocalFactorization(sym, spec.method, lv, uv,

@@ -1,0 +1,77 @@
+"""Run BASELINE.json's configs end to end on the GPU and print one JSON line
+each (setup times, iterations, solve time, true residual).
+
+    python tools/run_configs.py C1 C2ilu C3 C4
+"""
+import json
+import sys
+import time
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2304_04876_b200.decomposition import box_partition, decompose  # noqa: E402
+from paper_2304_04876_b200.krylov import KrylovConfig, gmres  # noqa: E402
+from paper_2304_04876_b200.local_solvers import SolverSpec  # noqa: E402
+from paper_2304_04876_b200.model_problems import (Grid3D, assemble_elasticity3d,  # noqa: E402
+                                                  assemble_laplace3d)
+from paper_2304_04876_b200.schwarz import SchwarzConfig, setup_numeric, setup_symbolic  # noqa: E402
+
+CONFIGS = {
+    # name: (kind, n, boxes, solver, ordering, precision)
+    "C1": ("laplace", 30, 2, SolverSpec("exact_lu"), "nested_dissection", "double"),
+    "C2": ("laplace", 128, 4, SolverSpec("fast_ilu", 0, 3, 5), "natural", "double"),
+    "C2ilu": ("laplace", 128, 4, SolverSpec("ilu_k", 0), "natural", "double"),
+    "C2single": ("laplace", 128, 4, SolverSpec("fast_ilu", 0, 3, 5), "natural", "single"),
+    "C3": ("elasticity", 64, 8, SolverSpec("exact_lu"), "nested_dissection", "double"),
+    "C4": ("laplace", 200, 5, SolverSpec("fast_ilu", 0, 3, 5), "natural", "single"),
+    "C4double": ("laplace", 200, 5, SolverSpec("fast_ilu", 0, 3, 5), "natural", "double"),
+    "C5_512": ("laplace", 128, 8, SolverSpec("fast_ilu", 0, 3, 5), "natural", "double"),
+}
+
+
+def run(name):
+    kind, n, p, spec, ordk, prec = CONFIGS[name]
+    t0 = time.perf_counter()
+    grid = Grid3D(n, n, n)
+    prob = assemble_laplace3d(grid) if kind == "laplace" else assemble_elasticity3d(grid)
+    dec = decompose(prob.a, box_partition(prob.grid, p, p, p), 1, "rgdsw")
+    t_in = time.perf_counter() - t0
+    cfg = SchwarzConfig(local=spec, ordering=ordk, precision=prec)
+    t0 = time.perf_counter()
+    skel = setup_symbolic(prob.a, dec, cfg)
+    t_sym = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    pre = setup_numeric(skel, prob.a, prob.nullspace)
+    torch.cuda.synchronize()
+    t_num = time.perf_counter() - t0
+    x_star = np.random.default_rng(0).standard_normal(prob.a.nrows)
+    b = prob.a @ x_star
+    bd = torch.from_numpy(b).cuda()
+    kc = KrylovConfig(variant="single_reduce")
+    gmres(prob.a, pre, bd, kc)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    x, rep = gmres(prob.a, pre, bd, kc)
+    e1.record()
+    torch.cuda.synchronize()
+    xh = x.cpu().numpy()
+    out = dict(config=name, n=prob.a.nrows, subdomains=p ** 3,
+               n_coarse=pre.coarse.a0.nrows if pre.coarse else 0,
+               setup_s=dict(inputs=t_in, symbolic=t_sym, numeric=t_num),
+               iterations=rep.iterations, converged=rep.converged,
+               solve_ms=e0.elapsed_time(e1), ms_per_iteration=e0.elapsed_time(e1) / max(rep.iterations, 1),
+               true_rel_residual=float(np.linalg.norm(b - prob.a @ xh) / np.linalg.norm(b)),
+               fill_nnz=int(sum(s.fill_nnz for s in skel.local_symbolics)))
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    for name in sys.argv[1:]:
+        try:
+            run(name)
+        except Exception as e:  # keep going through the list
+            print(json.dumps(dict(config=name, error=f"{type(e).__name__}: {e}")), flush=True)
