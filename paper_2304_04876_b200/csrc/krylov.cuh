@@ -1,11 +1,10 @@
 // GMRES vector kernels (krylov.py:260-361 single-reduce, 179-257 classic).
 //
 // * k_block_dot: the ONE fused reduction per single-reduce iteration,
-//   [V[:j]; v]^T [v, z] (krylov.py:290-300). A CTA stages a 1024-element
-//   tile of v and z in shared memory once; its warps then stream the basis
-//   rows of that tile with 16-byte loads (each row read exactly once per
-//   solve pass) against the staged tile. Few rows (norms, MGS dots): several
-//   warps split each row's tile. Deterministic: fixed grid, fixed tile
+//   [V[:j]; v]^T [v, z] (krylov.py:290-300). Each thread owns element pairs
+//   (grid-stride, 16-byte loads) and keeps all 2*rows running sums in
+//   registers, so every basis row is streamed exactly once with many
+//   independent loads in flight. Deterministic: fixed grid, fixed element
 //   assignment, fixed shuffle trees, and the last CTA to finish reduces the
 //   per-CTA partials in a fixed order (no second launch).
 // * k_sr_update: v[j], zm[j] and the speculative next candidate w in one
@@ -17,106 +16,125 @@ namespace gdsw {
 
 constexpr int KDOT_ROWS = 32;  // rows per block-dot launch (basis rows + self)
 constexpr int KDOT_THREADS = 256;
-constexpr int KDOT_TILE = 1024;
 constexpr int KDOT_W2 = 2 * KDOT_ROWS;
 
-// rows of the combined list [V[0..nv), v] restricted to [r0, r0 + nrc).
-// out[2*rr + {0,1}] = row . v, row . z  (rr = local row index)
-__global__ void __launch_bounds__(KDOT_THREADS, 3) k_block_dot(
+// rows of the combined list [V[0..nv), v] restricted to [r0, r0 + nrc),
+// nrc <= NR. out[2*rr + {0,1}] = row . v, row . z  (rr = local row index).
+// Each thread owns element pairs (grid-stride, 16-byte loads) and keeps
+// 2*NR running sums in registers: every basis row is read exactly once and
+// all NR row loads of a step are independent (deep memory-level
+// parallelism). One shuffle tree per sum at the end, per-CTA partials in
+// fixed slots, the last CTA reduces them in CTA order (deterministic).
+template <int NR>
+__global__ void __launch_bounds__(KDOT_THREADS, NR > 8 ? 1 : 2) k_block_dot(
     int64_t n, const double* __restrict__ V, int64_t ldv, int nv, int r0, int nrc,
     const double* __restrict__ v, const double* __restrict__ z, double* __restrict__ partial,
     double* __restrict__ out, unsigned* __restrict__ counter) {
-  __shared__ double red[KDOT_THREADS / 32][4][2];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NW = KDOT_THREADS / 32;
-  constexpr int KT = 256;      // elements per warp tile: 4 x 16-byte loads per lane
-  // S warps per row when rows are few (each on its own tiles), else up to 4
-  // rows per warp (all warps of the CTA on the same tile, v/z hit L1)
-  const int S = nrc >= 5 ? 1 : (nrc >= 3 ? 2 : (nrc == 2 ? 4 : 8));
-  const int slice = warp % S;
-  const double* rows[4];
-  int nq = 0;
-  if (S > 1) {
-    int rr = warp / S;
-    if (rr < nrc) {
-      int g = r0 + rr;
-      rows[nq++] = g < nv ? V + (int64_t)g * ldv : v;
-    }
-  } else {
-    for (int rr = warp; rr < nrc && nq < 4; rr += NW) {
-      int g = r0 + rr;
-      rows[nq++] = g < nv ? V + (int64_t)g * ldv : v;
-    }
-  }
-  double av[4] = {0, 0, 0, 0}, az[4] = {0, 0, 0, 0};
-  const int64_t ntiles = (n + KT - 1) / KT;
+  __shared__ double red[NW][2 * NR];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // rows q < nb come from V[r0 + q]; row nv - r0 (if in range) is v itself
+  const int nb = max(0, min(nrc, nv - r0));
+  const bool self = nv - r0 >= 0 && nv - r0 < nrc;
+  double av[NR], az[NR], as = 0.0, zs = 0.0;
+#pragma unroll
+  for (int q = 0; q < NR; ++q) av[q] = az[q] = 0.0;
   const bool vec = ((ldv & 1) == 0) && ((reinterpret_cast<uintptr_t>(V) & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(v) & 15) == 0) &&
                    ((reinterpret_cast<uintptr_t>(z) & 15) == 0);
-  for (int64_t t0 = (int64_t)blockIdx.x * S; t0 < ntiles; t0 += (int64_t)gridDim.x * S) {
-    const int64_t tile = t0 + slice;
-    if (tile >= ntiles || nq == 0) continue;
-    const int64_t base = tile * KT;
-    const int cnt = (int)(n - base < KT ? n - base : KT);
-    if (vec && cnt == KT) {
-      double2 pv[4], pz[4];
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nth = (int64_t)gridDim.x * blockDim.x;
+  const double* Vr = V ? V + (int64_t)r0 * ldv : V;
+  if (vec) {
+    const int64_t n2 = n >> 1;
+    const int32_t ld2 = (int32_t)(ldv >> 1);
+#pragma unroll 1
+    for (int64_t i = tid; i < n2; i += nth) {
+      const double2 pv = __ldg(reinterpret_cast<const double2*>(v) + i);
+      const double2 pz = z ? __ldg(reinterpret_cast<const double2*>(z) + i) : make_double2(0.0, 0.0);
+      const double2* pb = reinterpret_cast<const double2*>(Vr) + i;
+      // rows whose loads are in flight together (one CTA per SM above 8 rows:
+      // more loads per thread)
+      constexpr int G = NR <= 16 ? NR : NR / 2;
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int64_t e = base + 64 * t + 2 * lane;
-        pv[t] = __ldg(reinterpret_cast<const double2*>(v + e));
-        pz[t] = z ? __ldg(reinterpret_cast<const double2*>(z + e)) : make_double2(0.0, 0.0);
-      }
-      for (int q = 0; q < nq; ++q) {
-        double2 x[4];
+      for (int q0 = 0; q0 < NR; q0 += G) {
+        double2 x[G];
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-          x[t] = ldg_stream(reinterpret_cast<const double2*>(rows[q] + base + 64 * t + 2 * lane));
-        double a = 0.0, c = 0.0;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          a = fma(x[t].x, pv[t].x, a);
-          a = fma(x[t].y, pv[t].y, a);
-          c = fma(x[t].x, pz[t].x, c);
-          c = fma(x[t].y, pz[t].y, c);
+        for (int u = 0; u < G; ++u) {
+          if (q0 + u < nb) x[u] = ldg_stream(pb);
+          pb += ld2;
         }
-        av[q] += a;
-        az[q] += c;
-      }
-    } else {
-      for (int q = 0; q < nq; ++q) {
-        double a = 0.0, c = 0.0;
-        for (int e = lane; e < cnt; e += 32) {
-          const double x = rows[q][base + e];
-          a = fma(x, v[base + e], a);
-          if (z) c = fma(x, z[base + e], c);
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+          if (q0 + u < nb) {
+            av[q0 + u] = fma(x[u].y, pv.y, fma(x[u].x, pv.x, av[q0 + u]));
+            az[q0 + u] = fma(x[u].y, pz.y, fma(x[u].x, pz.x, az[q0 + u]));
+          }
         }
-        av[q] += a;
-        az[q] += c;
+      }
+      if (self) {
+        as = fma(pv.y, pv.y, fma(pv.x, pv.x, as));
+        zs = fma(pv.y, pz.y, fma(pv.x, pz.x, zs));
       }
     }
+    if ((n & 1) && tid == 0) {
+      const int64_t e = n - 1;
+      const double ve = v[e], ze = z ? z[e] : 0.0;
+      const double* pe = Vr + e;
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        if (q < nb) {
+          av[q] = fma(*pe, ve, av[q]);
+          az[q] = fma(*pe, ze, az[q]);
+        }
+        pe += ldv;
+      }
+      as = fma(ve, ve, as);
+      zs = fma(ve, ze, zs);
+    }
+  } else {
+#pragma unroll 1
+    for (int64_t e = tid; e < n; e += nth) {
+      const double ve = v[e], ze = z ? z[e] : 0.0;
+      const double* pe = Vr + e;
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        if (q < nb) {
+          const double x = *pe;
+          av[q] = fma(x, ve, av[q]);
+          az[q] = fma(x, ze, az[q]);
+        }
+        pe += ldv;
+      }
+      as = fma(ve, ve, as);
+      zs = fma(ve, ze, zs);
+    }
   }
-  for (int q = 0; q < 4; ++q) {
-    double a = warp_sum(av[q]);
-    double c = warp_sum(az[q]);
-    if (lane == 0) {
-      red[warp][q][0] = a;
-      red[warp][q][1] = c;
+  if (self) {  // the self row sits at slot nb
+#pragma unroll
+    for (int q = 0; q < NR; ++q)
+      if (q == nb) {
+        av[q] = as;
+        az[q] = zs;
+      }
+  }
+#pragma unroll
+  for (int q = 0; q < NR; ++q) {
+    if (q < nrc) {
+      const double a = warp_sum(av[q]);
+      const double c = warp_sum(az[q]);
+      if (lane == 0) {
+        red[warp][2 * q] = a;
+        red[warp][2 * q + 1] = c;
+      }
     }
   }
   __syncthreads();
-  for (int rr = threadIdx.x; rr < nrc; rr += KDOT_THREADS) {
-    double a = 0.0, c = 0.0;
-    if (S > 1) {
-      for (int w = rr * S; w < rr * S + S; ++w) {
-        a += red[w][0][0];
-        c += red[w][0][1];
-      }
-    } else {
-      a = red[rr % NW][rr / NW][0];
-      c = red[rr % NW][rr / NW][1];
-    }
-    partial[(int64_t)blockIdx.x * KDOT_W2 + 2 * rr] = a;
-    partial[(int64_t)blockIdx.x * KDOT_W2 + 2 * rr + 1] = c;
+  for (int k = threadIdx.x; k < 2 * nrc; k += KDOT_THREADS) {
+    double a = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) a += red[w][k];
+    partial[(int64_t)blockIdx.x * KDOT_W2 + k] = a;
   }
   // the last CTA reduces all per-CTA partials in a fixed order
   __shared__ bool last;
@@ -133,6 +151,25 @@ __global__ void __launch_bounds__(KDOT_THREADS, 3) k_block_dot(
     if (lane == 0) out[k] = s;
   }
   if (threadIdx.x == 0) *counter = 0u;
+}
+
+// host dispatch on the row-count bucket
+inline void launch_block_dot(unsigned grid, cudaStream_t s, int64_t n, const double* V, int64_t ldv,
+                             int nv, int r0, int nrc, const double* v, const double* z,
+                             double* partial, double* out, unsigned* counter) {
+  if (nrc <= 4)
+    k_block_dot<4><<<grid, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out, counter);
+  else if (nrc <= 8)
+    k_block_dot<8><<<grid, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out, counter);
+  else if (nrc <= 16)  // 32+ running sums: one CTA per SM (launch bound), half the grid
+    k_block_dot<16><<<(grid + 1) / 2, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out,
+                                                          counter);
+  else if (nrc <= 24)
+    k_block_dot<24><<<(grid + 1) / 2, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out,
+                                                          counter);
+  else
+    k_block_dot<32><<<(grid + 1) / 2, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out,
+                                                          counter);
 }
 
 // single-reduce update (krylov.py:346-351). coef = [a(0..j), p/delta(0..j),
