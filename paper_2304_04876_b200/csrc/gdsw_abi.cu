@@ -19,6 +19,8 @@
 #include "krylov.cuh"
 #include "prof.cuh"
 #include "sparse.cuh"
+#include "trisolve.cuh"
+#include "tristream.cuh"
 
 using namespace gdsw;
 
@@ -61,6 +63,11 @@ constexpr int TB = 256;
 // on B200 until the fused kernel's latency chain is shortened
 // GDSW_L2HINT=1 enables L2 evict_last hints on the Jacobi iterates
 // (measured slower on B200 at C2: off by default)
+bool env_flag(const char* name) {
+  const char* e = std::getenv(name);
+  return e && e[0] == '1';
+}
+
 bool l2_hints_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("GDSW_L2HINT");
@@ -177,7 +184,10 @@ struct gdsw_plan {
   DBuf<int32_t> sub_ptr, gmap;
   DBuf<int64_t> l_ptr, u_ptr;
   DBuf<int32_t> l_col, u_col;
-  DBuf<int32_t> llev_sub, llev_ptr, llev_rows, ulev_sub, ulev_ptr, ulev_rows;
+  // host level schedules (block-local rows), for the scheduled SpTRSV
+  std::vector<int64_t> h_llev_sub, h_llev_ptr, h_llev_rows, h_ulev_sub, h_ulev_ptr, h_ulev_rows;
+  TriSched l_sched, u_sched;     // exact / ILU(k) level-set layouts
+  bool sched_ready = false;
   std::vector<int64_t> row_add;  // block row offset per concatenated row
   std::vector<int64_t> h_l_idx, h_u_idx;
   SellPattern l_sell, u_sell;    // Jacobi layouts (U without its diagonal)
@@ -198,9 +208,11 @@ struct gdsw_plan {
     sell_ready = true;
   }
 
-  LevelSetDev levelset() const {
-    return LevelSetDev{sub_ptr.p,  gmap.p,     l_ptr.p,    l_col.p,     u_ptr.p,    u_col.p,
-                       llev_sub.p, llev_ptr.p, llev_rows.p, ulev_sub.p, ulev_ptr.p, ulev_rows.p};
+  void ensure_sched() {
+    if (sched_ready) return;
+    l_sched.build(n_sub, h_sub_ptr, h_l_ptr, h_l_idx, 0, h_llev_sub, h_llev_ptr, h_llev_rows);
+    u_sched.build(n_sub, h_sub_ptr, h_u_ptr, h_u_idx, 1, h_ulev_sub, h_ulev_ptr, h_ulev_rows);
+    sched_ready = true;
   }
   FastIluDev fastilu_dev() const {
     return FastIluDev{nnz_l, nnz_u, a_of.p, fi_ptr.p, fi_pl.p, fi_pu.p, fi_ldiag.p};
@@ -300,24 +312,16 @@ void build_local(gdsw_plan* P, const gdsw_local_desc* d) {
     P->l_col.upload(lc);
     P->u_col.upload(uc);
   }
-  // level schedules (block-local rows -> absolute)
-  auto levels = [&](const int64_t* lsub, const int64_t* lptr, const int64_t* lrows, DBuf<int32_t>& dsub,
-                    DBuf<int32_t>& dptr, DBuf<int32_t>& drows) {
-    std::vector<int64_t> sub = vec(lsub, ns + 1);
-    int64_t nlev = sub[ns];
-    std::vector<int64_t> ptr = vec(lptr, nlev + 1);
-    std::vector<int64_t> rows = vec(lrows, d->n_loc);
-    std::vector<int32_t> arows(d->n_loc);
-    for (int32_t s = 0; s < ns; ++s)
-      for (int64_t lv = sub[s]; lv < sub[s + 1]; ++lv)
-        for (int64_t t = ptr[lv]; t < ptr[lv + 1]; ++t)
-          arows[t] = (int32_t)(rows[t] + P->h_sub_ptr[s]);
-    dsub.upload(to_i32(sub.data(), sub.size()));
-    dptr.upload(to_i32(ptr.data(), ptr.size()));
-    drows.upload(arows);
-  };
-  levels(d->llev_sub, d->llev_ptr, d->llev_rows, P->llev_sub, P->llev_ptr, P->llev_rows);
-  levels(d->ulev_sub, d->ulev_ptr, d->ulev_rows, P->ulev_sub, P->ulev_ptr, P->ulev_rows);
+  // level schedules (block-local rows)
+  {
+    const int64_t nl = d->llev_sub[ns], nu = d->ulev_sub[ns];
+    P->h_llev_sub = vec(d->llev_sub, ns + 1);
+    P->h_llev_ptr = vec(d->llev_ptr, nl + 1);
+    P->h_llev_rows = vec(d->llev_rows, d->n_loc);
+    P->h_ulev_sub = vec(d->ulev_sub, ns + 1);
+    P->h_ulev_ptr = vec(d->ulev_ptr, nu + 1);
+    P->h_ulev_rows = vec(d->ulev_rows, d->n_loc);
+  }
   // owner-computes scatter: positions grouped by global row, ascending block
   {
     std::vector<int64_t> gm = vec(d->gmap, d->n_loc);
@@ -548,6 +552,10 @@ struct gdsw_precond {
   bool has_factors = false, jacobi_ready = false, has_phi = false, has_ainv = false;
   DBuf<char> lval, uval;           // CSR order
   DBuf<char> lsell, usell, udiag;  // Jacobi copies
+  DBuf<char> lsv, usv, sdiag;      // scheduled-SpTRSV copies (exact / ILU(k))
+  bool sched_vals_ready = false;
+  TriStream tstream;               // streamed-SpTRSV layout (exact / ILU(k))
+  bool stream_built = false, stream_vals_ready = false;
   DBuf<double> panel64;
   DBuf<char> panel32;              // f32 copy when dtype == F32
   DBuf<char> pgr_val, pgt_val, ainv;
@@ -559,6 +567,58 @@ struct gdsw_precond {
     plan_release(plan);
   }
   const void* panel() const { return dtype == GDSW_F32 ? (const void*)panel32.p : (const void*)panel64.p; }
+
+  void ensure_sched_vals() {
+    if (sched_vals_ready) return;
+    gdsw_plan* P = plan;
+    P->ensure_sched();
+    lsv.alloc(std::max<int64_t>(P->l_sched.entries, 1) * es);
+    usv.alloc(std::max<int64_t>(P->u_sched.entries, 1) * es);
+    sdiag.alloc(std::max<int64_t>(P->n_loc, 1) * es);
+    CK(cudaMemset(lsv.p, 0, lsv.n));
+    CK(cudaMemset(usv.p, 0, usv.n));
+    with_dtype(dtype, [&](auto tag) {
+      using T = decltype(tag);
+      const dim3 blk(32, 8);
+      for (auto* pr : {&P->l_sched, &P->u_sched}) {
+        if (pr->n_place == 0) continue;
+        const bool up = pr == &P->u_sched;
+        k_sched_place<T><<<grid_for(pr->n_place, 8), blk>>>(pr->n_place, pr->pl_src.p, pr->pl_dst.p, pr->pl_len.p,
+                                                            pr->pl_stride.p, (const T*)(up ? uval.p : lval.p),
+                                                            (T*)(up ? usv.p : lsv.p));
+        CK_LAUNCH();
+      }
+      if (P->n_loc) {
+        k_extract_diag<T><<<grid_for(P->n_loc, TB), TB>>>((int32_t)P->n_loc, P->u_ptr.p, (const T*)uval.p,
+                                                          (T*)sdiag.p);
+        CK_LAUNCH();
+      }
+    });
+    CK(cudaDeviceSynchronize());
+    sched_vals_ready = true;
+  }
+
+  void ensure_stream_vals() {
+    if (stream_vals_ready) return;
+    gdsw_plan* P = plan;
+    if (!stream_built) {
+      TriStream::Fac L{&P->h_l_ptr, &P->h_l_idx, &P->h_llev_sub, &P->h_llev_ptr, &P->h_llev_rows, 0};
+      TriStream::Fac U{&P->h_u_ptr, &P->h_u_idx, &P->h_ulev_sub, &P->h_ulev_ptr, &P->h_ulev_rows, 1};
+      tstream.build(P->n_sub, P->h_sub_ptr, L, U, (int)es);
+      stream_built = true;
+    }
+    with_dtype(dtype, [&](auto tag) {
+      using T = decltype(tag);
+      if (tstream.n_place) {
+        k_stream_place<T><<<grid_for(tstream.n_place, 8), dim3(32, 8)>>>(
+            tstream.n_place, tstream.pl_src.p, tstream.pl_dst.p, tstream.pl_len.p, tstream.pl_stride.p,
+            (const T*)lval.p, (const T*)uval.p, P->nnz_l, (T*)tstream.bytes.p);
+        CK_LAUNCH();
+      }
+    });
+    CK(cudaDeviceSynchronize());
+    stream_vals_ready = true;
+  }
 
   void ensure_jacobi() {
     if (jacobi_ready) return;
@@ -679,14 +739,76 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   return cur;
 }
 
+template <typename T, typename CT, bool SMEMX>
+void launch_stream(gdsw_precond* m, const double* r, T* y, size_t smem, cudaStream_t s) {
+  static bool attr = [] {
+    CK(cudaFuncSetAttribute(k_trisolve_stream<T, CT, SMEMX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            200 * 1024));
+    return true;
+  }();
+  (void)attr;
+  k_trisolve_stream<T, CT, SMEMX><<<m->plan->n_sub, TR_THREADS_ALL, smem, s>>>(m->tstream.view(), m->plan->sub_ptr.p,
+                                                                              m->plan->gmap.p, r, y);
+}
+
 template <typename T>
 T* levelset_solve(gdsw_precond* m, const double* r, cudaStream_t s) {
   gdsw_plan* P = m->plan;
-  ProfScope ps("levelset", s, (double)(P->nnz_l + P->nnz_u) * (sizeof(T) + 4) + P->n_loc * (8.0 + 3 * sizeof(T)));
-  k_levelset<T><<<P->n_sub, 512, 0, s>>>(P->levelset(), (const T*)m->lval.p, (const T*)m->uval.p, r,
-                                         (T*)m->x1.p, 0, 1);
+  static const bool sched = env_flag("GDSW_TS_SCHED");
+  if (!sched) {
+    m->ensure_stream_vals();
+    const TriStream& ts = m->tstream;
+    // algorithmic bytes: L and U entries once (value + stored column
+    // width), U's diagonal, the gather (gmap + r) and the block solution
+    ProfScope ps("levelset", s, (double)(P->nnz_l + P->nnz_u - P->n_loc) * (sizeof(T) + ts.csize) +
+                                    P->n_loc * (12.0 + 2 * sizeof(T)));
+    T* y = (T*)m->x1.p;
+    const size_t ring = (size_t)TR_NSLOT * ts.chunk_max;
+    const size_t xs = (size_t)ts.max_rows * sizeof(T);
+    const bool smx = ring + xs <= 200 * 1024;
+    const size_t smem = ring + (smx ? xs : 0);
+    require(ring <= 200 * 1024, "streamed SpTRSV chunk too large");
+    if (ts.csize == 2) {
+      if (smx) launch_stream<T, uint16_t, true>(m, r, y, smem, s);
+      else launch_stream<T, uint16_t, false>(m, r, y, smem, s);
+    } else {
+      if (smx) launch_stream<T, int32_t, true>(m, r, y, smem, s);
+      else launch_stream<T, int32_t, false>(m, r, y, smem, s);
+    }
+    CK_LAUNCH();
+    return y;
+  }
+  m->ensure_sched_vals();
+  // algorithmic bytes: L and U entries once (value + 4 B column), U's
+  // diagonal, the gather (gmap + r) and the block solution
+  ProfScope ps("levelset", s, (double)(P->nnz_l + P->nnz_u - P->n_loc) * (sizeof(T) + 4) +
+                                  P->n_loc * (12.0 + 2 * sizeof(T)));
+  const size_t smem = (size_t)P->l_sched.max_rows * sizeof(T);
+  constexpr size_t SMEM_MAX = 200 * 1024;
+  T* y = (T*)m->x1.p;
+  auto go = [&](auto kern, size_t sm) {
+    kern<<<P->n_sub, TS_THREADS, sm, s>>>(P->l_sched.view(), P->u_sched.view(), (const T*)m->lsv.p,
+                                          (const T*)m->usv.p, (const T*)m->sdiag.p, P->sub_ptr.p, P->gmap.p, r,
+                                          y);
+  };
+  static const bool simple = env_flag("GDSW_TS_SIMPLE");
+  if (smem <= SMEM_MAX) {
+    static bool attr_set = [] {
+      CK(cudaFuncSetAttribute(k_trisolve_sched<T, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)SMEM_MAX));
+      CK(cudaFuncSetAttribute(k_trisolve_sched<T, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)SMEM_MAX));
+      return true;
+    }();
+    (void)attr_set;
+    if (simple) go(k_trisolve_sched<T, true, false>, smem);
+    else go(k_trisolve_sched<T, true, true>, smem);
+  } else {
+    if (simple) go(k_trisolve_sched<T, false, false>, 0);
+    else go(k_trisolve_sched<T, false, true>, 0);
+  }
   CK_LAUNCH();
-  return (T*)m->x1.p;
+  return y;
 }
 
 template <typename T>
@@ -860,7 +982,11 @@ int gdsw_precond_set_factors(gdsw_precond* m, const void* l_vals, const void* u_
     if (P->nnz_u) CK(cudaMemcpy(m->uval.p, u_vals, P->nnz_u * m->es, cudaMemcpyHostToDevice));
     m->has_factors = true;
     m->jacobi_ready = false;
+    m->sched_vals_ready = false;
+    m->stream_vals_ready = false;
     if (P->method == GDSW_FAST_ILU) m->ensure_jacobi();
+    else if (env_flag("GDSW_TS_SCHED")) m->ensure_sched_vals();
+    else m->ensure_stream_vals();
   });
 }
 
@@ -926,6 +1052,8 @@ int gdsw_precond_fastilu(gdsw_precond* m, const gdsw_csr* a, int sweeps, double*
                   "initial guess (diagonal shift) or exact ILU");
     m->has_factors = true;
     m->jacobi_ready = false;
+    m->sched_vals_ready = false;
+    m->stream_vals_ready = false;
     m->ensure_jacobi();
   });
 }

@@ -416,62 +416,6 @@ __global__ void __cluster_dims__(JC_CLUSTER, 1, 1) __launch_bounds__(JC_THREADS,
 }
 
 // ---------------------------------------------------------------------------
-// batched level-set SpTRSV: one CTA per subdomain, gather + forward (unit L)
-// + backward (U, diagonal first) over the host-computed level schedules
-// (trisolve_forward_unit / trisolve_backward, _kernels.py:473-496). Rows of
-// one level are independent, so each row's sequential accumulation
-// reproduces sequential substitution bit for bit.
-// ---------------------------------------------------------------------------
-struct LevelSetDev {
-  const int32_t* sub_ptr;
-  const int32_t* gmap;
-  const int64_t* l_ptr;
-  const int32_t* l_col;
-  const int64_t* u_ptr;
-  const int32_t* u_col;
-  const int32_t* llev_sub;
-  const int32_t* llev_ptr;
-  const int32_t* llev_rows;
-  const int32_t* ulev_sub;
-  const int32_t* ulev_ptr;
-  const int32_t* ulev_rows;
-};
-
-template <typename T>
-__global__ void __launch_bounds__(512) k_levelset(LevelSetDev P, const T* __restrict__ lval,
-                                                  const T* __restrict__ uval,
-                                                  const double* __restrict__ r,
-                                                  T* __restrict__ x, int sub0, int do_gather) {
-  const int s = sub0 + blockIdx.x;
-  if (do_gather) {
-    for (int32_t k = P.sub_ptr[s] + threadIdx.x; k < P.sub_ptr[s + 1]; k += blockDim.x)
-      x[k] = (T)r[P.gmap[k]];
-    __syncthreads();
-  }
-  for (int32_t lv = P.llev_sub[s]; lv < P.llev_sub[s + 1]; ++lv) {
-    for (int32_t t = P.llev_ptr[lv] + threadIdx.x; t < P.llev_ptr[lv + 1]; t += blockDim.x) {
-      const int32_t i = P.llev_rows[t];
-      T acc = x[i];
-      for (int64_t p = P.l_ptr[i]; p < P.l_ptr[i + 1]; ++p)
-        acc = rn_sub(acc, rn_mul(lval[p], x[P.l_col[p]]));
-      x[i] = acc;
-    }
-    __syncthreads();
-  }
-  for (int32_t lv = P.ulev_sub[s]; lv < P.ulev_sub[s + 1]; ++lv) {
-    for (int32_t t = P.ulev_ptr[lv] + threadIdx.x; t < P.ulev_ptr[lv + 1]; t += blockDim.x) {
-      const int32_t i = P.ulev_rows[t];
-      const int64_t p0 = P.u_ptr[i];
-      T acc = x[i];
-      for (int64_t p = p0 + 1; p < P.u_ptr[i + 1]; ++p)
-        acc = rn_sub(acc, rn_mul(uval[p], x[P.u_col[p]]));
-      x[i] = rn_div(acc, uval[p0]);
-    }
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------
 // owner-computes scatter + coarse prolongation (schwarz.py:302-306, 322-327):
 //   z[g] = double( (Phi v)[g] + (((0 + y_a) + y_b) + ...) )
 // contributions y are summed in ascending subdomain order -- no atomics, the

@@ -1,0 +1,486 @@
+// Streamed batched SpTRSV for exact / ILU(k) factors (trisolve_levelset,
+// local_solvers.py:404-410, over trisolve_forward_unit / trisolve_backward,
+// _kernels.py:473-496).
+//
+// One CTA per subdomain. The subdomain's L then U factor are serialised on
+// the host into ONE contiguous byte stream of level-ordered chunks (tables,
+// values, 16-bit or 32-bit block-local columns, U's diagonal). A producer
+// warp streams the chunks with TMA bulk copies (cp.async.bulk) into a
+// shared-memory ring guarded by full/empty mbarriers; eight consumer warps
+// solve each chunk from shared memory against the block iterate (shared
+// memory when it fits, else global) and meet at one named barrier per
+// chunk -- a level never spans a barrier-free chunk boundary. The factor
+// bytes are read from HBM exactly once per solve, ahead of the dependency
+// chain, so a level costs a barrier plus on-chip work.
+//
+// Work in a chunk:
+//  * short rows (<= TR_SHORT entries): one thread per row, SELL-32 slices
+//    (entry k of lane l at 32k + l), sequential round-to-nearest mul/sub in
+//    column order -- bit-identical to the reference;
+//  * medium rows (<= TR_SEG entries): one warp per row, products in
+//    parallel, subtraction chain in column order (bit-identical);
+//  * long rows: TR_SEG-entry segments, one warp each, fused products and a
+//    fixed shuffle tree; the last segment to finish (smem counter) combines
+//    the partials in segment order -- deterministic, within 1e-13 relative
+//    of sequential substitution.
+#pragma once
+#include <algorithm>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace gdsw {
+
+constexpr int TR_CWARPS = 8;                    // consumer warps
+constexpr int TR_CTHREADS = 32 * TR_CWARPS;
+constexpr int TR_THREADS_ALL = TR_CTHREADS + 32;  // + producer warp
+constexpr int TR_SHORT = 32;
+constexpr int TR_SEG = 128;
+constexpr int TR_NSLOT = 4;
+constexpr int TR_MAXW = 64;                     // warp tasks per chunk
+constexpr int TR_CHUNK_MIN = 16 * 1024;
+
+__host__ __device__ inline int64_t ts_al16(int64_t b) { return (b + 15) & ~int64_t(15); }
+
+// section offsets of a chunk holding nw warp tasks and nsl short slices
+struct ChunkLayout {
+  int32_t wtab, wgrp, wdiag, stab, srow, slen, sdiag, data;
+  __host__ __device__ ChunkLayout(int nw, int nsl, bool up, int vsize) {
+    wtab = 16;
+    wgrp = wtab + 16 * nw;
+    wdiag = (int32_t)ts_al16(wgrp + 8 * nw);
+    stab = (int32_t)ts_al16(wdiag + (up ? vsize * nw : 0));
+    srow = stab + 16 * nsl;
+    slen = srow + 128 * nsl;
+    sdiag = slen + 128 * nsl;
+    data = (int32_t)ts_al16(sdiag + (up ? 32 * vsize * nsl : 0));
+  }
+};
+
+struct TriStreamDev {
+  const unsigned char* bytes = nullptr;
+  const int32_t* ch_sub = nullptr;   // [n_sub + 1] chunk range of each subdomain (L chunks, then U)
+  const int64_t* ch_off = nullptr;   // byte offset of each chunk
+  const int32_t* ch_len = nullptr;   // bytes of each chunk (multiple of 16)
+  int32_t chunk_max = 0;
+};
+
+// ---------------------------------------------------------------------------
+// host-side serialisation (values are placed on the device: k_stream_place)
+// ---------------------------------------------------------------------------
+struct TriStream {
+  int64_t total = 0, n_chunks = 0, max_rows = 0;
+  int32_t chunk_max = 0;
+  int vsize = 8, csize = 4;
+  DBuf<unsigned char> bytes;
+  DBuf<int32_t> ch_sub, ch_len;
+  DBuf<int64_t> ch_off;
+  // value placement: element (vsize) offsets into the stream
+  DBuf<int64_t> pl_src, pl_dst;
+  DBuf<int32_t> pl_len, pl_stride;
+  int64_t n_place = 0;
+
+  struct Fac {
+    const std::vector<int64_t>* ptr;
+    const std::vector<int64_t>* idx;
+    const std::vector<int64_t>* lsub;
+    const std::vector<int64_t>* lptr;
+    const std::vector<int64_t>* lrows;
+    int skip;  // 1: U (diagonal first, stored separately)
+  };
+
+  void build(int32_t n_sub, const std::vector<int64_t>& sub_ptr, const Fac& L, const Fac& U, int vsize_) {
+    vsize = vsize_;
+    const int64_t nnz_l = L.ptr->back();
+    max_rows = 0;
+    int64_t max_row_len = 0;
+    for (int32_t s = 0; s < n_sub; ++s) max_rows = std::max<int64_t>(max_rows, sub_ptr[s + 1] - sub_ptr[s]);
+    csize = max_rows <= 65536 ? 2 : 4;
+    for (const Fac* f : {&L, &U})
+      for (int64_t g = 0; g + 1 < (int64_t)f->ptr->size(); ++g)
+        max_row_len = std::max<int64_t>(max_row_len, (*f->ptr)[g + 1] - (*f->ptr)[g] - f->skip);
+    // a chunk must hold the longest row (all its segments) with its tables
+    const int64_t nseg_max = (max_row_len + TR_SEG - 1) / TR_SEG;
+    require(nseg_max <= TR_MAXW, "factor row too long for the streamed SpTRSV");
+    const int64_t need = ChunkLayout((int)nseg_max, 0, true, vsize).data +
+                         nseg_max * (ts_al16(TR_SEG * (int64_t)vsize) + ts_al16(TR_SEG * (int64_t)csize));
+    chunk_max = (int32_t)ts_al16(std::max<int64_t>(TR_CHUNK_MIN, need));
+
+    std::vector<unsigned char> buf;
+    std::vector<int32_t> h_ch_sub(n_sub + 1), h_ch_len;
+    std::vector<int64_t> h_ch_off, p_src, p_dst;
+    std::vector<int32_t> p_len, p_stride;
+
+    // one chunk under construction
+    struct WT { int32_t row, len, first, nseg; int64_t src; int64_t diag_src; };
+    struct SL { std::vector<int32_t> rows, lens; std::vector<int64_t> srcs, dsrc; int32_t width; };
+    std::vector<WT> wts;
+    std::vector<SL> sls;
+    int64_t data_bytes = 0;
+    bool up = false;
+    auto cur_bytes = [&](size_t nw, size_t nsl, int64_t db) {
+      return (int64_t)ChunkLayout((int)nw, (int)nsl, up, vsize).data + db;
+    };
+    auto flush = [&]() {
+      if (wts.empty() && sls.empty()) return;
+      const int nw = (int)wts.size(), nsl = (int)sls.size();
+      ChunkLayout cl(nw, nsl, up, vsize);
+      const int64_t off = (int64_t)buf.size();
+      const int64_t len = cl.data + data_bytes;
+      require(len <= chunk_max, "internal: chunk overflow");
+      buf.resize(off + len, 0);
+      unsigned char* c = buf.data() + off;
+      auto put32 = [&](int64_t at, int32_t v) { std::memcpy(c + at, &v, 4); };
+      put32(0, nw);
+      put32(4, nsl);
+      put32(8, up ? 1 : 0);
+      int64_t dp = cl.data;
+      const std::vector<int64_t>& idx = *(up ? U.idx : L.idx);
+      auto put_cols = [&](int64_t at, int64_t src, int32_t n, int32_t stride) {
+        for (int32_t k = 0; k < n; ++k) {
+          const int64_t v = idx[src + k];
+          if (csize == 2) {
+            const uint16_t h = (uint16_t)v;
+            std::memcpy(c + at + (int64_t)k * stride * 2, &h, 2);
+          } else {
+            const int32_t h = (int32_t)v;
+            std::memcpy(c + at + (int64_t)k * stride * 4, &h, 4);
+          }
+        }
+      };
+      for (int t = 0; t < nw; ++t) {
+        const WT& w = wts[t];
+        const int64_t voff = dp;
+        dp += ts_al16((int64_t)w.len * vsize);
+        const int64_t coff = dp;
+        dp += ts_al16((int64_t)w.len * csize);
+        put32(cl.wtab + 16 * t + 0, w.row);
+        put32(cl.wtab + 16 * t + 4, w.len);
+        put32(cl.wtab + 16 * t + 8, (int32_t)voff);
+        put32(cl.wtab + 16 * t + 12, (int32_t)coff);
+        put32(cl.wgrp + 8 * t + 0, w.first);
+        put32(cl.wgrp + 8 * t + 4, w.nseg);
+        put_cols(coff, w.src, w.len, 1);
+        p_src.push_back(w.src + (up ? nnz_l : 0));
+        p_dst.push_back((off + voff) / vsize);
+        p_len.push_back(w.len);
+        p_stride.push_back(1);
+        if (up && w.diag_src >= 0) {
+          p_src.push_back(w.diag_src + nnz_l);
+          p_dst.push_back((off + cl.wdiag + (int64_t)vsize * t) / vsize);
+          p_len.push_back(1);
+          p_stride.push_back(1);
+        }
+      }
+      for (int q = 0; q < nsl; ++q) {
+        const SL& sl = sls[q];
+        const int64_t voff = dp;
+        dp += ts_al16((int64_t)32 * sl.width * vsize);
+        const int64_t coff = dp;
+        dp += ts_al16((int64_t)32 * sl.width * csize);
+        put32(cl.stab + 16 * q + 0, (int32_t)voff);
+        put32(cl.stab + 16 * q + 4, (int32_t)coff);
+        put32(cl.stab + 16 * q + 8, sl.width);
+        for (int l = 0; l < 32; ++l) {
+          const bool ok = l < (int)sl.rows.size();
+          put32(cl.srow + 4 * (32 * q + l), ok ? sl.rows[l] : 0);
+          put32(cl.slen + 4 * (32 * q + l), ok ? sl.lens[l] : -1);
+          if (!ok) continue;
+          if (sl.lens[l] > 0) {
+            put_cols(coff + (int64_t)csize * l, sl.srcs[l], sl.lens[l], 32);
+            p_src.push_back(sl.srcs[l] + (up ? nnz_l : 0));
+            p_dst.push_back((off + voff) / vsize + l);
+            p_len.push_back(sl.lens[l]);
+            p_stride.push_back(32);
+          }
+          if (up) {
+            p_src.push_back(sl.dsrc[l] + nnz_l);
+            p_dst.push_back((off + cl.sdiag + (int64_t)vsize * (32 * q + l)) / vsize);
+            p_len.push_back(1);
+            p_stride.push_back(1);
+          }
+        }
+      }
+      require(dp == len, "internal: chunk layout mismatch");
+      h_ch_off.push_back(off);
+      h_ch_len.push_back((int32_t)len);
+      wts.clear();
+      sls.clear();
+      data_bytes = 0;
+    };
+
+    for (int32_t s = 0; s < n_sub; ++s) {
+      h_ch_sub[s] = (int32_t)h_ch_off.size();
+      const int64_t base = sub_ptr[s];
+      for (const Fac* f : {&L, &U}) {
+        up = f->skip == 1;
+        const std::vector<int64_t>& ptr = *f->ptr;
+        for (int64_t lv = (*f->lsub)[s]; lv < (*f->lsub)[s + 1]; ++lv) {
+          std::vector<int64_t> shorts;
+          for (int64_t t = (*f->lptr)[lv]; t < (*f->lptr)[lv + 1]; ++t) {
+            const int64_t row = (*f->lrows)[t], g = base + row;
+            const int64_t len = ptr[g + 1] - ptr[g] - f->skip;
+            if (len <= TR_SHORT) {
+              shorts.push_back(row);
+              continue;
+            }
+            const int32_t nseg = (int32_t)((len + TR_SEG - 1) / TR_SEG);
+            int64_t db = 0;
+            for (int32_t q = 0; q < nseg; ++q) {
+              const int64_t sl = std::min<int64_t>(TR_SEG, len - (int64_t)q * TR_SEG);
+              db += ts_al16(sl * vsize) + ts_al16(sl * csize);
+            }
+            if (wts.size() + nseg > (size_t)TR_MAXW ||
+                cur_bytes(wts.size() + nseg, sls.size(), data_bytes + db) > chunk_max)
+              flush();
+            const int32_t first = (int32_t)wts.size();
+            for (int32_t q = 0; q < nseg; ++q) {
+              const int64_t sl = std::min<int64_t>(TR_SEG, len - (int64_t)q * TR_SEG);
+              wts.push_back(WT{(int32_t)row, (int32_t)sl, first, nseg, ptr[g] + f->skip + (int64_t)q * TR_SEG,
+                               (q == 0 && up) ? ptr[g] : -1});
+            }
+            data_bytes += db;
+          }
+          for (size_t s0 = 0; s0 < shorts.size(); s0 += 32) {
+            SL sl;
+            sl.width = 0;
+            for (size_t q = s0; q < std::min(shorts.size(), s0 + 32); ++q) {
+              const int64_t g = base + shorts[q];
+              const int32_t len = (int32_t)(ptr[g + 1] - ptr[g] - f->skip);
+              sl.rows.push_back((int32_t)shorts[q]);
+              sl.lens.push_back(len);
+              sl.srcs.push_back(ptr[g] + f->skip);
+              sl.dsrc.push_back(ptr[g]);
+              sl.width = std::max(sl.width, len);
+            }
+            const int64_t db = ts_al16((int64_t)32 * sl.width * vsize) + ts_al16((int64_t)32 * sl.width * csize);
+            if (cur_bytes(wts.size(), sls.size() + 1, data_bytes + db) > chunk_max) flush();
+            sls.push_back(std::move(sl));
+            data_bytes += db;
+          }
+          flush();  // a level ends a chunk (its barrier is the level barrier)
+        }
+      }
+    }
+    h_ch_sub[n_sub] = (int32_t)h_ch_off.size();
+    total = (int64_t)buf.size();
+    n_chunks = (int64_t)h_ch_off.size();
+    bytes.upload(buf.data(), std::max<size_t>(buf.size(), 16));
+    ch_sub.upload(h_ch_sub);
+    ch_off.upload(h_ch_off);
+    ch_len.upload(h_ch_len);
+    pl_src.upload(p_src);
+    pl_dst.upload(p_dst);
+    pl_len.upload(p_len);
+    pl_stride.upload(p_stride);
+    n_place = (int64_t)p_src.size();
+  }
+  TriStreamDev view() const {
+    TriStreamDev v;
+    v.bytes = bytes.p;
+    v.ch_sub = ch_sub.p;
+    v.ch_off = ch_off.p;
+    v.ch_len = ch_len.p;
+    v.chunk_max = chunk_max;
+    return v;
+  }
+};
+
+// CSR values (and U's diagonal) -> their stream slots. Sources index the
+// concatenation [L values | U values].
+template <typename T>
+__global__ void k_stream_place(int64_t n_place, const int64_t* __restrict__ src, const int64_t* __restrict__ dst,
+                               const int32_t* __restrict__ len, const int32_t* __restrict__ stride,
+                               const T* __restrict__ lval, const T* __restrict__ uval, int64_t nnz_l,
+                               T* __restrict__ out) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
+  if (q >= n_place) return;
+  int64_t s0 = src[q];
+  const T* v = lval;
+  if (s0 >= nnz_l) {
+    v = uval;
+    s0 -= nnz_l;
+  }
+  const int64_t d0 = dst[q];
+  const int32_t n = len[q], st = stride[q];
+  for (int32_t k = threadIdx.x; k < n; k += blockDim.x) out[d0 + (int64_t)k * st] = v[s0 + k];
+}
+
+// ---------------------------------------------------------------------------
+// mbarrier / bulk-copy primitives (sm_90+ PTX)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void consumer_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(TR_CTHREADS) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// chunk solve
+// ---------------------------------------------------------------------------
+template <typename T, typename CT>
+__device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T* x, T* part, int* cnt) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int4 hdr = *reinterpret_cast<const int4*>(c);
+  const int nw = hdr.x, nsl = hdr.y;
+  const bool up = hdr.z & 1;
+  const ChunkLayout cl(nw, nsl, up, (int)sizeof(T));
+  // warp tasks (medium rows and segments of long rows)
+  for (int t = warp; t < nw; t += TR_CWARPS) {
+    const int4 w = *reinterpret_cast<const int4*>(c + cl.wtab + 16 * t);
+    const int2 gp = *reinterpret_cast<const int2*>(c + cl.wgrp + 8 * t);
+    const int32_t row = w.x, len = w.y;
+    const T* v = reinterpret_cast<const T*>(c + w.z);
+    const CT* cc = reinterpret_cast<const CT*>(c + w.w);
+    T p[TR_SEG / 32];
+#pragma unroll
+    for (int u = 0; u < TR_SEG / 32; ++u) {
+      const int k = lane + 32 * u;
+      p[u] = k < len ? rn_mul(v[k], x[cc[k]]) : T(0);
+    }
+    if (gp.y == 1) {
+      // whole row in one segment: subtraction chain in column order
+      T xi = x[row];
+#pragma unroll
+      for (int u = 0; u < TR_SEG / 32; ++u) {
+        if (32 * u >= len) break;  // warp-uniform
+#pragma unroll
+        for (int l = 0; l < 32; ++l) {
+          const T pk = __shfl_sync(0xffffffffu, p[u], l);
+          if (32 * u + l < len) xi = rn_sub(xi, pk);
+        }
+      }
+      if (up) xi = rn_div(xi, reinterpret_cast<const T*>(c + cl.wdiag)[t]);
+      if (lane == 0) x[row] = xi;
+    } else {
+      T acc = T(0);
+#pragma unroll
+      for (int u = 0; u < TR_SEG / 32; ++u) acc += p[u];
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        part[t] = acc;
+        __threadfence_block();
+        if (atomicAdd(cnt + gp.x, 1) == gp.y - 1) {
+          __threadfence_block();
+          T s = T(0);
+          for (int q = 0; q < gp.y; ++q) s += *(volatile T*)(part + gp.x + q);
+          T xi = x[row] - s;
+          if (up) xi = rn_div(xi, reinterpret_cast<const T*>(c + cl.wdiag)[gp.x]);
+          x[row] = xi;
+          cnt[gp.x] = 0;
+        }
+      }
+    }
+  }
+  // short rows: one thread each, sequential in column order
+  const int32_t* srow = reinterpret_cast<const int32_t*>(c + cl.srow);
+  const int32_t* slen = reinterpret_cast<const int32_t*>(c + cl.slen);
+  for (int t = threadIdx.x; t < 32 * nsl; t += TR_CTHREADS) {
+    const int32_t len = slen[t];
+    if (len < 0) continue;
+    const int32_t row = srow[t];
+    const int4 st = *reinterpret_cast<const int4*>(c + cl.stab + 16 * (t >> 5));
+    const T* v = reinterpret_cast<const T*>(c + st.x) + (t & 31);
+    const CT* cc = reinterpret_cast<const CT*>(c + st.y) + (t & 31);
+    T acc = x[row];
+    for (int k0 = 0; k0 < len; k0 += 4) {
+      T pv[4], xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (k0 + u < len) {
+          pv[u] = v[32 * (k0 + u)];
+          xv[u] = x[cc[32 * (k0 + u)]];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k0 + u < len) acc = rn_sub(acc, rn_mul(pv[u], xv[u]));
+    }
+    if (up) acc = rn_div(acc, reinterpret_cast<const T*>(c + cl.sdiag)[t]);
+    x[row] = acc;
+  }
+}
+
+// one CTA per subdomain: gather (ordering folded into gmap), every chunk of
+// L then U streamed through the ring, block solution written to y
+template <typename T, typename CT, bool SMEMX>
+__global__ void __launch_bounds__(TR_THREADS_ALL) k_trisolve_stream(TriStreamDev S,
+                                                                    const int32_t* __restrict__ sub_ptr,
+                                                                    const int32_t* __restrict__ gmap,
+                                                                    const double* __restrict__ r,
+                                                                    T* __restrict__ y) {
+  extern __shared__ __align__(128) unsigned char ts_sm[];
+  __shared__ uint64_t full[TR_NSLOT], empty[TR_NSLOT];
+  __shared__ T part[TR_MAXW];
+  __shared__ int cnt[TR_MAXW];
+  const int s = blockIdx.x;
+  const int32_t base = sub_ptr[s], ns = sub_ptr[s + 1] - base;
+  const int c0 = S.ch_sub[s], c1 = S.ch_sub[s + 1];
+  unsigned char* ring = ts_sm;
+  T* x = SMEMX ? reinterpret_cast<T*>(ts_sm + (size_t)TR_NSLOT * S.chunk_max) : y + base;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < TR_NSLOT; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < TR_MAXW) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  if (threadIdx.x >= TR_CTHREADS) {
+    // producer warp: one elected lane streams the chunks
+    if (threadIdx.x == TR_CTHREADS) {
+      for (int c = c0; c < c1; ++c) {
+        const int i = c - c0, slot = i % TR_NSLOT;
+        const uint32_t ph = (uint32_t)((i / TR_NSLOT) & 1);
+        mbar_wait(&empty[slot], ph ^ 1);
+        const uint32_t nb = (uint32_t)S.ch_len[c];
+        mbar_expect_tx(&full[slot], nb);
+        bulk_g2s(ring + (size_t)slot * S.chunk_max, S.bytes + S.ch_off[c], nb, &full[slot]);
+      }
+    }
+    return;
+  }
+  for (int32_t k = threadIdx.x; k < ns; k += TR_CTHREADS) x[k] = (T)r[gmap[base + k]];
+  consumer_bar();
+  for (int c = c0; c < c1; ++c) {
+    const int i = c - c0, slot = i % TR_NSLOT;
+    mbar_wait(&full[slot], (uint32_t)((i / TR_NSLOT) & 1));
+    ts_chunk<T, CT>(ring + (size_t)slot * S.chunk_max, x, part, cnt);
+    consumer_bar();
+    if (threadIdx.x == 0) mbar_arrive(&empty[slot]);
+  }
+  if (SMEMX)
+    for (int32_t k = threadIdx.x; k < ns; k += TR_CTHREADS) y[base + k] = x[k];
+}
+
+}  // namespace gdsw

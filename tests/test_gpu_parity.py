@@ -68,8 +68,22 @@ def test_spmv_bitwise_against_oracle():
         assert np.array_equal(yy.cpu().numpy(), want - want)
 
 
+TS_CHAIN = 128   # trisolve.cuh: rows up to this length keep the sequential order
+LONG_ROW_TOL = 1e-13
+
+
+def _max_row_len(sym):
+    lu = np.diff(sym.u_ptr) - 1
+    ll = np.diff(sym.l_ptr)
+    return int(max(ll.max(initial=0), lu.max(initial=0)))
+
+
 @pytest.mark.parametrize("name", sorted(CASES))
 def test_local_solves_bitwise_against_oracle(name):
+    """Bit-identical to sequential substitution whenever every factor row has
+    <= TS_CHAIN entries (Jacobi sweeps, ILU(k), small exact blocks); rows of
+    dense separators beyond that use a fixed-tree warp reduction and are
+    compared at 1e-13 relative."""
     torch = _torch()
     prob, dec, cfg, skel, pre = setup_case(name)
     ore = O.OracleSchwarz(prob.a, dec, cfg, prob.nullspace if cfg.use_coarse else None,
@@ -86,7 +100,10 @@ def test_local_solves_bitwise_against_oracle(name):
         got = np.empty_like(want)
         got[sym.ordering.perm] = y[off:off + dofs.size]
         off += dofs.size
-        assert np.array_equal(got, want), f"subdomain {i}"
+        if cfg.local.method == "fast_ilu" or _max_row_len(sym) <= TS_CHAIN:
+            assert np.array_equal(got, want), f"subdomain {i}"
+        else:
+            assert np.abs(got - want).max() <= LONG_ROW_TOL * np.abs(want).max(), f"subdomain {i}"
 
 
 @pytest.mark.parametrize("name", [n for n in sorted(CASES) if CASES[n][4] == "fast_ilu"])
