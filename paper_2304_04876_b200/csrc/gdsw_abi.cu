@@ -111,8 +111,12 @@ template <typename T>
 void spmv_T(const gdsw_csr* a, const T* x, const T* yin, T* y, int mode, double alpha, double beta,
             cudaStream_t s) {
   if (a->nrows == 0) return;
-  k_sell_spmv<T><<<grid_for(a->nrows, TB), TB, 0, s>>>(a->pat.view(), (const T*)a->sell_val.p, x,
-                                                        yin, y, mode, (T)alpha, (T)beta);
+  if (a->pat.has16)
+    k_sell_spmv<T, true><<<grid_for(a->nrows, TB), TB, 0, s>>>(a->pat.view(), (const T*)a->sell_val.p, x,
+                                                              yin, y, mode, (T)alpha, (T)beta);
+  else
+    k_sell_spmv<T, false><<<grid_for(a->nrows, TB), TB, 0, s>>>(a->pat.view(), (const T*)a->sell_val.p, x,
+                                                               yin, y, mode, (T)alpha, (T)beta);
   CK_LAUNCH();
 }
 }  // namespace
@@ -156,7 +160,7 @@ int gdsw_csr_spmv(const gdsw_csr* a, const void* x, void* y, double alpha, doubl
                   void* stream) {
   return guarded([&] {
     int mode = (alpha == 1.0 && beta == 0.0) ? 0 : 2;
-    ProfScope ps("spmv", S(stream), (double)a->nnz * (esize(a->dtype) + 4) + (a->nrows + 1) * 4.0 +
+    ProfScope ps("spmv", S(stream), (double)a->nnz * (esize(a->dtype) + (a->pat.has16 ? 2 : 4)) + (a->nrows + 1) * 2.0 +
                                         2.0 * a->nrows * esize(a->dtype));
     with_dtype(a->dtype, [&](auto tag) {
       using T = decltype(tag);
@@ -649,7 +653,7 @@ namespace {
 
 // FastSpTRSV: `iters` Jacobi iterates on L then U; returns the buffer
 // holding the block solutions
-template <typename T, bool HINT>
+template <typename T, bool HINT, bool D16>
 T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   gdsw_plan* P = m->plan;
   const int32_t n = (int32_t)P->n_loc;
@@ -658,8 +662,9 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   T* X2 = (T*)m->x2.p;
   SellDev L = P->l_sell.view(), U = P->u_sell.view();
   const unsigned g = grid_for(n, TB);
-  const double lbytes = (double)P->nnz_l * (sizeof(T) + 4) + n * (2.0 + 3 * sizeof(T));
-  const double ubytes = (double)(P->nnz_u - n) * (sizeof(T) + 4) + n * (2.0 + 3 * sizeof(T));
+  const double cb = D16 ? 2.0 : 4.0;  // stored column bytes per entry
+  const double lbytes = (double)P->nnz_l * (sizeof(T) + cb) + n * (2.0 + 3 * sizeof(T));
+  const double ubytes = (double)(P->nnz_u - n) * (sizeof(T) + cb) + n * (2.0 + 3 * sizeof(T));
   if (jacobi_fused_enabled() && iters >= 1) {
     // one cluster per subdomain, all iterates in one launch. Algorithmic
     // bytes: both factors once (SELL values + columns + row lengths), U's
@@ -687,14 +692,14 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   } else {
     {
       ProfScope ps("gather_jacobi_lower", s, lbytes + n * (12.0 - sizeof(T)));
-      k_gather_jacobi_lower<T, HINT><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, P->gmap.p, r, B, X1);
+      k_gather_jacobi_lower<T, HINT, D16><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, P->gmap.p, r, B, X1);
       CK_LAUNCH();
     }
     T* cur = X1;
     T* oth = X2;
     for (int t = 2; t < iters - 1; ++t) {
       ProfScope ps("jacobi_lower", s, lbytes);
-      k_jacobi_lower<T, HINT><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth);
+      k_jacobi_lower<T, HINT, D16><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth);
       CK_LAUNCH();
       std::swap(cur, oth);
     }
@@ -703,7 +708,7 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
       T* X3 = (T*)m->x3.p;
       {
         ProfScope ps("jacobi_lower_diag", s, lbytes + n * 2.0 * sizeof(T));
-        k_jacobi_lower_diag<T, HINT><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth,
+        k_jacobi_lower_diag<T, HINT, D16><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth,
                                                 (const T*)m->udiag.p, X3);
         CK_LAUNCH();
       }
@@ -712,7 +717,7 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
       T* Hf = cur;  // B and cur are free now
       for (int t = 1; t < iters; ++t) {
         ProfScope ps("jacobi_upper", s, ubytes + n * (double)sizeof(T));
-        k_jacobi_upper<T, HINT><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, Gf, Hf);
+        k_jacobi_upper<T, HINT, D16><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, Gf, Hf);
         CK_LAUNCH();
         std::swap(Gf, Hf);
       }
@@ -732,7 +737,7 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   T* oth = H;
   for (int t = 1; t < iters; ++t) {
     ProfScope ps("jacobi_upper", s, ubytes + n * (double)sizeof(T));
-    k_jacobi_upper<T, HINT><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, cur, oth);
+    k_jacobi_upper<T, HINT, D16><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, cur, oth);
     CK_LAUNCH();
     std::swap(cur, oth);
   }
@@ -740,15 +745,15 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
 }
 
 template <typename T, typename CT, bool SMEMX>
-void launch_stream(gdsw_precond* m, const double* r, T* y, size_t smem, cudaStream_t s) {
+void launch_stream(gdsw_precond* m, const double* r, T* y, int32_t ring, size_t smem, cudaStream_t s) {
   static bool attr = [] {
     CK(cudaFuncSetAttribute(k_trisolve_stream<T, CT, SMEMX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            200 * 1024));
+                            220 * 1024));
     return true;
   }();
   (void)attr;
-  k_trisolve_stream<T, CT, SMEMX><<<m->plan->n_sub, TR_THREADS_ALL, smem, s>>>(m->tstream.view(), m->plan->sub_ptr.p,
-                                                                              m->plan->gmap.p, r, y);
+  k_trisolve_stream<T, CT, SMEMX><<<m->plan->n_sub, TR_THREADS_ALL, smem, s>>>(
+      m->tstream.view(), ring, m->plan->sub_ptr.p, m->plan->gmap.p, r, y);
 }
 
 template <typename T>
@@ -763,17 +768,26 @@ T* levelset_solve(gdsw_precond* m, const double* r, cudaStream_t s) {
     ProfScope ps("levelset", s, (double)(P->nnz_l + P->nnz_u - P->n_loc) * (sizeof(T) + ts.csize) +
                                     P->n_loc * (12.0 + 2 * sizeof(T)));
     T* y = (T*)m->x1.p;
-    const size_t ring = (size_t)TR_NSLOT * ts.chunk_max;
-    const size_t xs = (size_t)ts.max_rows * sizeof(T);
-    const bool smx = ring + xs <= 200 * 1024;
-    const size_t smem = ring + (smx ? xs : 0);
-    require(ring <= 200 * 1024, "streamed SpTRSV chunk too large");
+    // shared memory per CTA: the iterate goes to shared memory when it
+    // leaves a ring of at least 4 chunks
+    static const int64_t ring_env = [] {
+      const char* e = std::getenv("GDSW_TS_BUDGET_KB");
+      return e ? (int64_t)std::atoi(e) * 1024 : (int64_t)0;
+    }();
+    // measured on B200: a 64 KB budget beats larger rings (C1, C3-sized
+    // blocks and C2 ILU(0) all faster than at 100 or 220 KB)
+    const int64_t budget = ring_env ? ring_env : 64 * 1024;
+    const int64_t xs = ts.max_rows * (int64_t)sizeof(T);
+    const bool smx = budget - xs >= 4LL * ts.chunk_max;
+    const int64_t ring = std::max<int64_t>(2LL * ts.chunk_max, ((smx ? budget - xs : budget) & ~int64_t(15)));
+    const size_t smem = (size_t)ring + (smx ? (size_t)xs : 0);
+    require(smem <= 220 * 1024, "streamed SpTRSV chunk too large");
     if (ts.csize == 2) {
-      if (smx) launch_stream<T, uint16_t, true>(m, r, y, smem, s);
-      else launch_stream<T, uint16_t, false>(m, r, y, smem, s);
+      if (smx) launch_stream<T, uint16_t, true>(m, r, y, (int32_t)ring, smem, s);
+      else launch_stream<T, uint16_t, false>(m, r, y, (int32_t)ring, smem, s);
     } else {
-      if (smx) launch_stream<T, int32_t, true>(m, r, y, smem, s);
-      else launch_stream<T, int32_t, false>(m, r, y, smem, s);
+      if (smx) launch_stream<T, int32_t, true>(m, r, y, (int32_t)ring, smem, s);
+      else launch_stream<T, int32_t, false>(m, r, y, (int32_t)ring, smem, s);
     }
     CK_LAUNCH();
     return y;
@@ -817,7 +831,10 @@ T* local_solve(gdsw_precond* m, const double* r, int jacobi_iters, cudaStream_t 
   if (jacobi_iters > 0 || P->method == GDSW_FAST_ILU) {
     m->ensure_jacobi();
     const int it = jacobi_iters > 0 ? jacobi_iters : m->iters;
-    return l2_hints_enabled() ? jacobi_solve<T, true>(m, r, it, s) : jacobi_solve<T, false>(m, r, it, s);
+    const bool d16 = P->l_sell.has16 && P->u_sell.has16;
+    if (l2_hints_enabled())
+      return d16 ? jacobi_solve<T, true, true>(m, r, it, s) : jacobi_solve<T, true, false>(m, r, it, s);
+    return d16 ? jacobi_solve<T, false, true>(m, r, it, s) : jacobi_solve<T, false, false>(m, r, it, s);
   }
   return levelset_solve<T>(m, r, s);
 }

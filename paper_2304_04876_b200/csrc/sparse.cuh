@@ -20,7 +20,17 @@ struct SellDev {
   const int64_t* slice_off = nullptr;  // [n_slices + 1]
   const uint16_t* row_len = nullptr;   // [n_rows]
   const int32_t* col = nullptr;        // [padded nnz]
+  const int16_t* d16 = nullptr;        // [padded nnz] col - row, when every |col - row| < 2^15
 };
+
+// column of SELL entry q of row i: 16-bit row-relative offsets when the
+// pattern allows it (stencil-like and block-local factor patterns: 10 bytes
+// per fp64 entry instead of 12), else absolute int32
+template <bool D16>
+__device__ __forceinline__ int32_t sell_col(const SellDev& M, int32_t i, int64_t q) {
+  if (D16) return i + (int32_t)ldg_stream(M.d16 + q);
+  return ldg_stream(M.col + q);
+}
 
 // host-side SELL pattern builder from a CSR pattern whose column indices are
 // shifted by col_add (absolute positions in the concatenated vector)
@@ -30,6 +40,8 @@ struct SellPattern {
   DBuf<int64_t> slice_off;
   DBuf<uint16_t> row_len;
   DBuf<int32_t> col;
+  DBuf<int16_t> d16;
+  bool has16 = false;
   DBuf<int64_t> csr_ptr;  // CSR row pointers, for value placement
   // rows_offdiag_skip: number of leading entries of each CSR row to drop
   // (1 = U's diagonal, stored first)
@@ -51,18 +63,25 @@ struct SellPattern {
     }
     padded = off[ns];
     std::vector<int32_t> c(padded, 0);
+    std::vector<int16_t> d(padded, 0);
+    has16 = true;
     for (int64_t i = 0; i < n; ++i) {
       int64_t base = off[i / 32] + (i % 32);
       for (int64_t k = 0; k < len[i]; ++k) {
         int64_t v = idx[ptr[i] + skip_first + k] + col_add_per_row[i];
         require(v >= 0 && v <= INT32_MAX, "column exceeds int32");
         c[base + 32 * k] = (int32_t)v;
+        const int64_t dl = v - i;
+        if (dl < -32768 || dl > 32767) has16 = false;
+        d[base + 32 * k] = (int16_t)dl;
       }
       // padding stays column 0 (never read: loops stop at row_len)
     }
     slice_off.upload(off);
     row_len.upload(len);
     col.upload(c);
+    if (has16) d16.upload(d);
+    else d16.release();
     std::vector<int64_t> p(ptr, ptr + n + 1);
     csr_ptr.upload(p);
   }
@@ -72,6 +91,7 @@ struct SellPattern {
     v.slice_off = slice_off.p;
     v.row_len = row_len.p;
     v.col = col.p;
+    v.d16 = has16 ? d16.p : nullptr;
     return v;
   }
 };
@@ -108,9 +128,9 @@ struct LdCg {  // written by other CTAs of the same kernel: L2 only
 };
 
 // SUB: acc -= v*x (triangular sweeps); else acc += v*x (SpMV)
-template <typename T, typename TX, bool SUB, typename XL>
+template <typename T, typename TX, bool SUB, typename XL, bool D16>
 __device__ __forceinline__ T sell_row(T acc, int64_t base, int len, const T* __restrict__ val,
-                                      const int32_t* __restrict__ col, const TX* x) {
+                                      const SellDev& M, int32_t i, const TX* x) {
   for (int k0 = 0; k0 < len; k0 += SELL_U) {
     int32_t c[SELL_U];
     T v[SELL_U];
@@ -118,7 +138,7 @@ __device__ __forceinline__ T sell_row(T acc, int64_t base, int len, const T* __r
     for (int u = 0; u < SELL_U; ++u) {
       if (k0 + u < len) {
         const int64_t q = base + 32 * (int64_t)(k0 + u);
-        c[u] = ldg_stream(col + q);
+        c[u] = sell_col<D16>(M, i, q);
         v[u] = ldg_stream(val + q);
       }
     }
@@ -137,7 +157,7 @@ __device__ __forceinline__ T sell_row(T acc, int64_t base, int len, const T* __r
 // ---------------------------------------------------------------------------
 // SpMV: y = A x (mode 0), y = yin - A x (mode 1), y = alpha A x + beta yin (2)
 // ---------------------------------------------------------------------------
-template <typename T>
+template <typename T, bool D16>
 __global__ void __launch_bounds__(256) k_sell_spmv(SellDev A, const T* __restrict__ val,
                                                    const T* __restrict__ x,
                                                    const T* __restrict__ yin,
@@ -146,7 +166,7 @@ __global__ void __launch_bounds__(256) k_sell_spmv(SellDev A, const T* __restric
   if (i >= A.n_rows) return;
   const int64_t base = A.slice_off[i >> 5] + (i & 31);
   const int len = A.row_len[i];
-  const T acc = sell_row<T, T, false, LdNc>(T(0), base, len, val, A.col, x);
+  const T acc = sell_row<T, T, false, LdNc, D16>(T(0), base, len, val, A, i, x);
   if (mode == 0) {
     y[i] = acc;
   } else if (mode == 1) {
@@ -174,7 +194,7 @@ struct VecIO {
   }
 };
 
-template <typename T, bool HINT>
+template <typename T, bool HINT, bool D16>
 __global__ void __launch_bounds__(256) k_jacobi_lower(SellDev L, const T* __restrict__ lval,
                                                       const T* __restrict__ b,
                                                       const T* __restrict__ x,
@@ -187,13 +207,13 @@ __global__ void __launch_bounds__(256) k_jacobi_lower(SellDev L, const T* __rest
   T acc = io.ld(b + i);
   for (int k = 0; k < len; ++k) {
     const int64_t q = base + 32 * (int64_t)k;
-    acc = rn_sub(acc, rn_mul(ldg_stream(lval + q), io.ld(x + ldg_stream(L.col + q))));
+    acc = rn_sub(acc, rn_mul(ldg_stream(lval + q), io.ld(x + sell_col<D16>(L, i, q))));
   }
   io.st(xn + i, acc);
 }
 
 // x_new = D^-1 (b - (U - D) x)  (U off-diagonal part in SELL, D separate)
-template <typename T, bool HINT>
+template <typename T, bool HINT, bool D16>
 __global__ void __launch_bounds__(256) k_jacobi_upper(SellDev U, const T* __restrict__ uval,
                                                       const T* __restrict__ diag,
                                                       const T* __restrict__ b,
@@ -207,14 +227,14 @@ __global__ void __launch_bounds__(256) k_jacobi_upper(SellDev U, const T* __rest
   T acc = io.ld(b + i);
   for (int k = 0; k < len; ++k) {
     const int64_t q = base + 32 * (int64_t)k;
-    acc = rn_sub(acc, rn_mul(ldg_stream(uval + q), io.ld(x + ldg_stream(U.col + q))));
+    acc = rn_sub(acc, rn_mul(ldg_stream(uval + q), io.ld(x + sell_col<D16>(U, i, q))));
   }
   io.st(xn + i, rn_div(acc, io.ld(diag + i)));
 }
 
 // last L sweep fused with the first U iterate: writes both the L result F
 // and y1 = F / diag (saves one pass over the vectors)
-template <typename T, bool HINT>
+template <typename T, bool HINT, bool D16>
 __global__ void __launch_bounds__(256) k_jacobi_lower_diag(SellDev L, const T* __restrict__ lval,
                                                            const T* __restrict__ b,
                                                            const T* __restrict__ x,
@@ -229,7 +249,7 @@ __global__ void __launch_bounds__(256) k_jacobi_lower_diag(SellDev L, const T* _
   T f = io.ld(b + i);
   for (int k = 0; k < len; ++k) {
     const int64_t q = base + 32 * (int64_t)k;
-    f = rn_sub(f, rn_mul(ldg_stream(lval + q), io.ld(x + ldg_stream(L.col + q))));
+    f = rn_sub(f, rn_mul(ldg_stream(lval + q), io.ld(x + sell_col<D16>(L, i, q))));
   }
   io.st(xn + i, f);
   io.st(y1 + i, rn_div(f, io.ld(diag + i)));
@@ -253,7 +273,7 @@ __global__ void k_gather(int32_t n, const int32_t* __restrict__ gmap, const doub
 
 // gather fused with the first Jacobi L sweep: writes b = T(r[gmap]) and the
 // second iterate b - (L - I) b in one pass over L
-template <typename T, bool HINT>
+template <typename T, bool HINT, bool D16>
 __global__ void __launch_bounds__(256) k_gather_jacobi_lower(SellDev L,
                                                              const T* __restrict__ lval,
                                                              const int32_t* __restrict__ gmap,
@@ -276,7 +296,7 @@ __global__ void __launch_bounds__(256) k_gather_jacobi_lower(SellDev L,
     for (int u = 0; u < SELL_U; ++u) {
       if (k0 + u < len) {
         const int64_t q = base + 32 * (int64_t)(k0 + u);
-        c[u] = ldg_stream(L.col + q);
+        c[u] = sell_col<D16>(L, i, q);
         v[u] = ldg_stream(lval + q);
       }
     }
@@ -334,7 +354,7 @@ __device__ __forceinline__ void jc_rows(const SellDev& M, const T* __restrict__ 
       const int32_t ic = ok ? i : lo;
       const int64_t base = M.slice_off[ic >> 5] + (ic & 31);
       const int len = ok ? M.row_len[ic] : 0;
-      acc[m] = sell_row<T, T, true, LdCg>(ok ? __ldcg(b + ic) : T(0), base, len, val, M.col, x);
+      acc[m] = sell_row<T, T, true, LdCg, false>(ok ? __ldcg(b + ic) : T(0), base, len, val, M, ic, x);
     }
 #pragma unroll
     for (int m = 0; m < JC_ILP; ++m) {

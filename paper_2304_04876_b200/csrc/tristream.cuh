@@ -36,7 +36,6 @@ constexpr int TR_CTHREADS = 32 * TR_CWARPS;
 constexpr int TR_THREADS_ALL = TR_CTHREADS + 32;  // + producer warp
 constexpr int TR_SHORT = 32;
 constexpr int TR_SEG = 128;
-constexpr int TR_NSLOT = 4;
 constexpr int TR_MAXW = 64;                     // warp tasks per chunk
 constexpr int TR_CHUNK_MIN = 16 * 1024;
 
@@ -431,24 +430,29 @@ __device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T*
 }
 
 // one CTA per subdomain: gather (ordering folded into gmap), every chunk of
-// L then U streamed through the ring, block solution written to y
+// L then U streamed through a byte ring (chunks packed back to back, up to
+// TR_NT in flight; a chunk never wraps), block solution written to y
+constexpr int TR_NT = 16;
+
 template <typename T, typename CT, bool SMEMX>
-__global__ void __launch_bounds__(TR_THREADS_ALL) k_trisolve_stream(TriStreamDev S,
+__global__ void __launch_bounds__(TR_THREADS_ALL) k_trisolve_stream(TriStreamDev S, int32_t ring_bytes,
                                                                     const int32_t* __restrict__ sub_ptr,
                                                                     const int32_t* __restrict__ gmap,
                                                                     const double* __restrict__ r,
                                                                     T* __restrict__ y) {
   extern __shared__ __align__(128) unsigned char ts_sm[];
-  __shared__ uint64_t full[TR_NSLOT], empty[TR_NSLOT];
+  __shared__ uint64_t full[TR_NT], empty[TR_NT];
+  __shared__ int32_t pos[TR_NT], foot[TR_NT];
   __shared__ T part[TR_MAXW];
   __shared__ int cnt[TR_MAXW];
   const int s = blockIdx.x;
   const int32_t base = sub_ptr[s], ns = sub_ptr[s + 1] - base;
   const int c0 = S.ch_sub[s], c1 = S.ch_sub[s + 1];
+  const int nch = c1 - c0;
   unsigned char* ring = ts_sm;
-  T* x = SMEMX ? reinterpret_cast<T*>(ts_sm + (size_t)TR_NSLOT * S.chunk_max) : y + base;
+  T* x = SMEMX ? reinterpret_cast<T*>(ts_sm + ring_bytes) : y + base;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < TR_NSLOT; ++i) {
+    for (int i = 0; i < TR_NT; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
@@ -457,27 +461,56 @@ __global__ void __launch_bounds__(TR_THREADS_ALL) k_trisolve_stream(TriStreamDev
   if (threadIdx.x < TR_MAXW) cnt[threadIdx.x] = 0;
   __syncthreads();
   if (threadIdx.x >= TR_CTHREADS) {
-    // producer warp: one elected lane streams the chunks
-    if (threadIdx.x == TR_CTHREADS) {
-      for (int c = c0; c < c1; ++c) {
-        const int i = c - c0, slot = i % TR_NSLOT;
-        const uint32_t ph = (uint32_t)((i / TR_NSLOT) & 1);
-        mbar_wait(&empty[slot], ph ^ 1);
-        const uint32_t nb = (uint32_t)S.ch_len[c];
-        mbar_expect_tx(&full[slot], nb);
-        bulk_g2s(ring + (size_t)slot * S.chunk_max, S.bytes + S.ch_off[c], nb, &full[slot]);
+    // producer warp: the chunk table is read 32 entries at a time, one
+    // window ahead; lane 0 issues the copies
+    const int lane = threadIdx.x & 31;
+    int64_t off_c = 0, off_n = 0;
+    int32_t len_c = 0, len_n = 0;
+    if (lane < nch) {
+      off_n = S.ch_off[c0 + lane];
+      len_n = S.ch_len[c0 + lane];
+    }
+    int head = 0, inflight = 0, oldest = 0;
+    for (int i = 0; i < nch; ++i) {
+      if ((i & 31) == 0) {
+        off_c = off_n;
+        len_c = len_n;
+        if (i + 32 + lane < nch) {
+          off_n = S.ch_off[c0 + i + 32 + lane];
+          len_n = S.ch_len[c0 + i + 32 + lane];
+        }
       }
+      const int64_t off = __shfl_sync(0xffffffffu, off_c, i & 31);
+      const int32_t len = __shfl_sync(0xffffffffu, len_c, i & 31);
+      if (lane == 0) {
+        const int t = i % TR_NT;
+        const int start = head + len <= ring_bytes ? head : 0;
+        const int fp = len + (start == 0 && head != 0 ? ring_bytes - head : 0);
+        // retire consumed chunks until the ticket and the bytes are free
+        while (oldest < i && (i - oldest >= TR_NT || inflight + fp > ring_bytes)) {
+          mbar_wait(&empty[oldest % TR_NT], (uint32_t)((oldest / TR_NT) & 1));
+          inflight -= foot[oldest % TR_NT];
+          ++oldest;
+        }
+        pos[t] = start;
+        foot[t] = fp;
+        inflight += fp;
+        head = start + len;
+        mbar_expect_tx(&full[t], (uint32_t)len);
+        bulk_g2s(ring + start, S.bytes + off, (uint32_t)len, &full[t]);
+      }
+      __syncwarp();
     }
     return;
   }
   for (int32_t k = threadIdx.x; k < ns; k += TR_CTHREADS) x[k] = (T)r[gmap[base + k]];
   consumer_bar();
-  for (int c = c0; c < c1; ++c) {
-    const int i = c - c0, slot = i % TR_NSLOT;
-    mbar_wait(&full[slot], (uint32_t)((i / TR_NSLOT) & 1));
-    ts_chunk<T, CT>(ring + (size_t)slot * S.chunk_max, x, part, cnt);
+  for (int i = 0; i < nch; ++i) {
+    const int t = i % TR_NT;
+    mbar_wait(&full[t], (uint32_t)((i / TR_NT) & 1));
+    ts_chunk<T, CT>(ring + pos[t], x, part, cnt);
     consumer_bar();
-    if (threadIdx.x == 0) mbar_arrive(&empty[slot]);
+    if (threadIdx.x == 0) mbar_arrive(&empty[t]);
   }
   if (SMEMX)
     for (int32_t k = threadIdx.x; k < ns; k += TR_CTHREADS) y[base + k] = x[k];
