@@ -21,6 +21,7 @@
 #include "sparse.cuh"
 #include "trisolve.cuh"
 #include "tristream.cuh"
+#include "jacobi_flow.cuh"
 
 using namespace gdsw;
 
@@ -544,8 +545,22 @@ extern "C" int gdsw_plan_destroy(gdsw_plan* p) {
 // ===========================================================================
 // numeric preconditioner
 // ===========================================================================
+// work decomposition of the dataflow FastSpTRSV (jacobi_flow.cuh)
+struct FlowPlan {
+  int iters = 0, rpt = 0;
+  int32_t n_chunks = 0, n_groups = 0, n_sweeps = 0;
+  int64_t n_items = 0;
+  int grid = 0;
+  unsigned epoch = 0;
+  unsigned long long ticket_base = 0;
+  DBuf<int32_t> sub_chunk0, sub_row0, sub_reach, group_sub0;
+  DBuf<unsigned long long> ticket;
+  DBuf<unsigned> done;      // [n_sweeps * n_chunks] epoch stamps
+};
+
 struct gdsw_precond {
   gdsw_plan* plan = nullptr;
+  std::unique_ptr<FlowPlan> flow;
   std::unique_ptr<CoarsePlan> cp;
   gdsw_dist* dist = nullptr;         // sharded layout (not owned)
   DBuf<double> part_ext, recv_ext;   // reverse-halo partial sums (ext-local)
@@ -653,6 +668,136 @@ namespace {
 
 // FastSpTRSV: `iters` Jacobi iterates on L then U; returns the buffer
 // holding the block solutions
+// GDSW_JACOBI_FLOW=1: all sweeps in one persistent dataflow launch with
+// L2-resident subdomain groups (jacobi_flow.cuh). Measured on B200 at C2:
+// HBM traffic per apply drops from ~1.29 GB to ~0.33 GB, but the launch is
+// bound by the per-item dependent-load chain (309 us vs 270 us for the
+// per-sweep launches), so it is off by default.
+bool jacobi_flow_enabled() { return env_flag("GDSW_JACOBI_FLOW"); }
+
+// group subdomains so one group's factors + iterates fit the L2 budget
+template <typename T, bool D16, int RPT>
+FlowPlan* ensure_flow(gdsw_precond* m, int iters) {
+  constexpr int ROWS = JF_THREADS * RPT;
+  if (m->flow && m->flow->iters == iters && m->flow->rpt == RPT) return m->flow.get();
+  gdsw_plan* P = m->plan;
+  require(P->n_sub <= JF_MAXSUB, "too many subdomains for the dataflow FastSpTRSV");
+  auto F = std::make_unique<FlowPlan>();
+  F->iters = iters;
+  F->rpt = RPT;
+  F->n_sweeps = 2 * iters - 2;
+  require(F->n_sweeps <= JF_MAXSW, "too many Jacobi iterates for the dataflow kernel");
+  static const double budget = [] {
+    const char* e = std::getenv("GDSW_FLOW_MB");
+    return (e ? std::atof(e) : 80.0) * 1e6;
+  }();
+  const double cb = D16 ? 2.0 : 4.0;
+  std::vector<int32_t> sc0(P->n_sub + 1, 0), srow0(P->n_sub + 1, 0), reach(P->n_sub, 0), gsub0{0};
+  double ws = 0.0;
+  int32_t nch = 0;
+  for (int32_t sd = 0; sd < P->n_sub; ++sd) {
+    const int64_t r0 = P->h_sub_ptr[sd], r1 = P->h_sub_ptr[sd + 1];
+    const double nnz = (double)(P->h_l_ptr[r1] - P->h_l_ptr[r0]) + (double)(P->h_u_ptr[r1] - P->h_u_ptr[r0]);
+    const double b = nnz * (sizeof(T) + cb) + (double)(r1 - r0) * (4.0 + 5.0 * sizeof(T));
+    if (sd > gsub0.back() && ws + b > budget) {
+      gsub0.push_back(sd);
+      ws = 0.0;
+    }
+    ws += b;
+    sc0[sd] = nch;
+    srow0[sd] = (int32_t)r0;
+    nch += (int32_t)((r1 - r0 + ROWS - 1) / ROWS);
+    // reach: how many chunks away a row's columns can be (block-local)
+    int64_t K = 0;
+    for (int64_t i = r0; i < r1; ++i) {
+      const int64_t ci = (i - r0) / ROWS;
+      for (int64_t q = P->h_l_ptr[i]; q < P->h_l_ptr[i + 1]; ++q) K = std::max<int64_t>(K, ci - P->h_l_idx[q] / ROWS);
+      for (int64_t q = P->h_u_ptr[i]; q < P->h_u_ptr[i + 1]; ++q) K = std::max<int64_t>(K, P->h_u_idx[q] / ROWS - ci);
+    }
+    reach[sd] = (int32_t)K;
+    require(2 * K + 1 <= JF_THREADS, "factor reach too wide for the dataflow FastSpTRSV");
+  }
+  sc0[P->n_sub] = nch;
+  srow0[P->n_sub] = (int32_t)P->h_sub_ptr[P->n_sub];
+  gsub0.push_back(P->n_sub);
+  F->n_groups = (int32_t)gsub0.size() - 1;
+  require(F->n_groups <= JF_MAXGRP, "too many subdomain groups for the dataflow FastSpTRSV");
+  F->n_chunks = nch;
+  F->n_items = (int64_t)F->n_sweeps * nch;
+  F->sub_chunk0.upload(sc0);
+  F->sub_row0.upload(srow0);
+  F->sub_reach.upload(reach);
+  F->group_sub0.upload(gsub0);
+  F->ticket.alloc(1);
+  F->ticket.zero();
+  F->done.alloc(std::max<int64_t>((int64_t)F->n_sweeps * F->n_chunks, 1));
+  F->done.zero();
+  int nb = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_jacobi_flow<T, D16, RPT>, JF_THREADS, 0));
+  F->grid = std::max(1, nb) * num_sms();
+  CK(cudaDeviceSynchronize());
+  m->flow = std::move(F);
+  return m->flow.get();
+}
+
+// all sweeps in one launch; same buffer rotation as jacobi_solve
+template <typename T, bool D16, int RPT>
+T* jacobi_flow_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
+  gdsw_plan* P = m->plan;
+  FlowPlan* F = ensure_flow<T, D16, RPT>(m, iters);
+  T* B = (T*)m->xb.p;
+  T* X1 = (T*)m->x1.p;
+  T* X2 = (T*)m->x2.p;
+  T* X3 = (T*)m->x3.p;
+  JfPlan J{};
+  J.L = P->l_sell.view();
+  J.U = P->u_sell.view();
+  J.sub_chunk0 = F->sub_chunk0.p;
+  J.sub_row0 = F->sub_row0.p;
+  J.sub_reach = F->sub_reach.p;
+  J.group_sub0 = F->group_sub0.p;
+  J.n_sub = P->n_sub;
+  J.rows_per_chunk = JF_THREADS * RPT;
+  J.gmap = P->gmap.p;
+  J.n_groups = F->n_groups;
+  J.n_chunks = F->n_chunks;
+  J.n_sweeps = F->n_sweeps;
+  J.n_items = F->n_items;
+  // every launch consumes exactly n_items + grid tickets; done stamps carry
+  // the launch epoch, so nothing is reset between launches
+  J.ticket = F->ticket.p;
+  J.ticket_base = F->ticket_base;
+  F->ticket_base += (unsigned long long)F->n_items + (unsigned long long)F->grid;
+  J.done = F->done.p;
+  J.epoch = ++F->epoch;
+  int t = 0;
+  J.sw[t++] = JfSweep{0, nullptr, X1, nullptr, B};
+  T* cur = X1;
+  T* oth = X2;
+  for (int k = 2; k < iters - 1; ++k) {
+    J.sw[t++] = JfSweep{1, cur, oth, B, nullptr};
+    std::swap(cur, oth);
+  }
+  J.sw[t++] = JfSweep{2, cur, oth, B, X3};
+  T* Fv = oth;
+  T* Gf = X3;
+  T* Hf = cur;
+  for (int k = 1; k < iters; ++k) {
+    J.sw[t++] = JfSweep{3, Gf, Hf, Fv, nullptr};
+    std::swap(Gf, Hf);
+  }
+  require(t == F->n_sweeps, "internal: dataflow sweep count");
+  const double n = (double)P->n_loc, cb = D16 ? 2.0 : 4.0;
+  // algorithmic bytes of the fused launch: both factors once (values +
+  // stored columns + row lengths), U's diagonal, the gather and the result
+  ProfScope ps("jacobi_flow", s, (double)P->nnz_l * (sizeof(T) + cb) + (double)(P->nnz_u - P->n_loc) * (sizeof(T) + cb) +
+                                     n * (4.0 + sizeof(T)) + n * 12.0 + n * sizeof(T));
+  k_jacobi_flow<T, D16, RPT><<<F->grid, JF_THREADS, 0, s>>>(J, (const T*)m->lsell.p, (const T*)m->usell.p,
+                                                      (const T*)m->udiag.p, r);
+  CK_LAUNCH();
+  return Gf;
+}
+
 template <typename T, bool HINT, bool D16>
 T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   gdsw_plan* P = m->plan;
@@ -832,6 +977,17 @@ T* local_solve(gdsw_precond* m, const double* r, int jacobi_iters, cudaStream_t 
     m->ensure_jacobi();
     const int it = jacobi_iters > 0 ? jacobi_iters : m->iters;
     const bool d16 = P->l_sell.has16 && P->u_sell.has16;
+    if (jacobi_flow_enabled() && it >= 3 && !jacobi_fused_enabled()) {
+      static const int rpt = [] {
+        const char* e = std::getenv("GDSW_FLOW_RPT");
+        return e ? std::atoi(e) : 2;
+      }();
+      if (rpt == 1)
+        return d16 ? jacobi_flow_solve<T, true, 1>(m, r, it, s) : jacobi_flow_solve<T, false, 1>(m, r, it, s);
+      if (rpt == 4)
+        return d16 ? jacobi_flow_solve<T, true, 4>(m, r, it, s) : jacobi_flow_solve<T, false, 4>(m, r, it, s);
+      return d16 ? jacobi_flow_solve<T, true, 2>(m, r, it, s) : jacobi_flow_solve<T, false, 2>(m, r, it, s);
+    }
     if (l2_hints_enabled())
       return d16 ? jacobi_solve<T, true, true>(m, r, it, s) : jacobi_solve<T, true, false>(m, r, it, s);
     return d16 ? jacobi_solve<T, false, true>(m, r, it, s) : jacobi_solve<T, false, false>(m, r, it, s);
