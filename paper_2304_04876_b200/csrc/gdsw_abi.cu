@@ -100,7 +100,7 @@ struct gdsw_csr {
       using T = decltype(tag);
       k_csr_to_sell<T, T><<<grid_for(nrows, TB), TB>>>(
           (int32_t)nrows, pat.csr_ptr.p, pat.slice_off.p, (const T*)csr_val.p, (T*)sell_val.p, 0,
-          (T*)nullptr);
+          (T*)nullptr, pat.uw);
       CK_LAUNCH();
     });
     CK(cudaDeviceSynchronize());
@@ -652,11 +652,11 @@ struct gdsw_precond {
       using T = decltype(tag);
       k_csr_to_sell<T, T><<<grid_for(P->n_loc, TB), TB>>>((int32_t)P->n_loc, P->l_sell.csr_ptr.p,
                                                          P->l_sell.slice_off.p, (const T*)lval.p,
-                                                         (T*)lsell.p, 0, (T*)nullptr);
+                                                         (T*)lsell.p, 0, (T*)nullptr, P->l_sell.uw);
       CK_LAUNCH();
       k_csr_to_sell<T, T><<<grid_for(P->n_loc, TB), TB>>>((int32_t)P->n_loc, P->u_sell.csr_ptr.p,
                                                          P->u_sell.slice_off.p, (const T*)uval.p,
-                                                         (T*)usell.p, 1, (T*)udiag.p);
+                                                         (T*)usell.p, 1, (T*)udiag.p, P->u_sell.uw);
       CK_LAUNCH();
     });
     CK(cudaDeviceSynchronize());

@@ -74,7 +74,7 @@ __device__ __forceinline__ void jf_rows(const SellDev& M, const T* __restrict__ 
 #pragma unroll
   for (int u = 0; u < JF_RPT; ++u) {
     const int32_t i = rows[u];
-    base[u] = ok[u] ? M.slice_off[i >> 5] + (i & 31) : 0;
+    base[u] = ok[u] ? sell_base(M, i) : 0;
     len[u] = ok[u] ? (int)M.row_len[i] : 0;
   }
 #pragma unroll

@@ -21,7 +21,17 @@ struct SellDev {
   const uint16_t* row_len = nullptr;   // [n_rows]
   const int32_t* col = nullptr;        // [padded nnz]
   const int16_t* d16 = nullptr;        // [padded nnz] col - row, when every |col - row| < 2^15
+  int32_t uw = 0;                      // every slice padded to this width (<= SELL_UW), else 0
 };
+
+constexpr int SELL_UW = 8;  // widest pattern stored with uniform slice width
+
+// first SELL slot of row i: arithmetic for uniform-width layouts (no
+// dependent slice-offset load), else from slice_off
+__device__ __forceinline__ int64_t sell_base(const SellDev& M, int32_t i) {
+  if (M.uw) return (int64_t)(i >> 5) * 32 * M.uw + (i & 31);
+  return M.slice_off[i >> 5] + (i & 31);
+}
 
 // column of SELL entry q of row i: 16-bit row-relative offsets when the
 // pattern allows it (stencil-like and block-local factor patterns: 10 bytes
@@ -42,6 +52,7 @@ struct SellPattern {
   DBuf<int32_t> col;
   DBuf<int16_t> d16;
   bool has16 = false;
+  int32_t uw = 0;
   DBuf<int64_t> csr_ptr;  // CSR row pointers, for value placement
   // rows_offdiag_skip: number of leading entries of each CSR row to drop
   // (1 = U's diagonal, stored first)
@@ -56,10 +67,19 @@ struct SellPattern {
       require(l >= 0 && l < 65536, "row too long for the SELL layout");
       len[i] = (uint16_t)l;
     }
+    int64_t wmax = 0;
     for (int64_t s = 0; s < ns; ++s) {
       int64_t w = 0;
       for (int64_t i = s * 32; i < std::min<int64_t>(n, s * 32 + 32); ++i) w = std::max<int64_t>(w, len[i]);
       off[s + 1] = off[s] + 32 * w;
+      wmax = std::max(wmax, w);
+    }
+    // uniform width when narrow and the extra padding is small: the slot of
+    // a row is then computed, not loaded
+    uw = 0;
+    if (wmax > 0 && wmax <= SELL_UW && 32 * wmax * ns <= off[ns] + off[ns] / 8) {
+      uw = (int32_t)wmax;
+      for (int64_t s = 0; s <= ns; ++s) off[s] = 32 * wmax * s;
     }
     padded = off[ns];
     std::vector<int32_t> c(padded, 0);
@@ -92,6 +112,7 @@ struct SellPattern {
     v.row_len = row_len.p;
     v.col = col.p;
     v.d16 = has16 ? d16.p : nullptr;
+    v.uw = uw;
     return v;
   }
 };
@@ -101,10 +122,10 @@ struct SellPattern {
 template <typename T, typename TS>
 __global__ void k_csr_to_sell(int32_t n, const int64_t* __restrict__ ptr,
                               const int64_t* __restrict__ slice_off, const TS* __restrict__ src,
-                              T* __restrict__ dst, int skip, T* __restrict__ diag_out) {
+                              T* __restrict__ dst, int skip, T* __restrict__ diag_out, int32_t uw) {
   int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  int64_t base = slice_off[i >> 5] + (i & 31);
+  int64_t base = uw ? (int64_t)(i >> 5) * 32 * uw + (i & 31) : slice_off[i >> 5] + (i & 31);
   int64_t p0 = ptr[i], p1 = ptr[i + 1];
   if (skip && diag_out) diag_out[i] = (T)src[p0];
   for (int64_t p = p0 + skip, k = 0; p < p1; ++p, ++k) dst[base + 32 * k] = (T)src[p];
@@ -128,9 +149,35 @@ struct LdCg {  // written by other CTAs of the same kernel: L2 only
 };
 
 // SUB: acc -= v*x (triangular sweeps); else acc += v*x (SpMV)
+// uniform-width row: every slot's column and value load is issued at once
+// (no dependence on the row length), then the gathers of the row's own
+// entries, then the ordered accumulation
+template <typename T, typename TX, bool SUB, typename XL, bool D16, int MW = SELL_UW>
+__device__ __forceinline__ T sell_row_uniform(T acc, int64_t base, int len, const T* __restrict__ val,
+                                              const SellDev& M, int32_t i, const TX* x) {
+  int32_t c[MW];
+  T v[MW], xv[MW];
+#pragma unroll
+  for (int k = 0; k < MW; ++k) {
+    if (k < M.uw) {
+      const int64_t q = base + 32 * (int64_t)k;
+      c[k] = sell_col<D16>(M, i, q);
+      v[k] = ldg_stream(val + q);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < MW; ++k)
+    if (k < len) xv[k] = (T)XL::ld(x + c[k]);
+#pragma unroll
+  for (int k = 0; k < MW; ++k)
+    if (k < len) acc = SUB ? rn_sub(acc, rn_mul(v[k], xv[k])) : rn_add(acc, rn_mul(v[k], xv[k]));
+  return acc;
+}
+
 template <typename T, typename TX, bool SUB, typename XL, bool D16>
 __device__ __forceinline__ T sell_row(T acc, int64_t base, int len, const T* __restrict__ val,
                                       const SellDev& M, int32_t i, const TX* x) {
+  if (M.uw) return sell_row_uniform<T, TX, SUB, XL, D16>(acc, base, len, val, M, i, x);
   for (int k0 = 0; k0 < len; k0 += SELL_U) {
     int32_t c[SELL_U];
     T v[SELL_U];
@@ -164,7 +211,7 @@ __global__ void __launch_bounds__(256) k_sell_spmv(SellDev A, const T* __restric
                                                    T* __restrict__ y, int mode, T alpha, T beta) {
   int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= A.n_rows) return;
-  const int64_t base = A.slice_off[i >> 5] + (i & 31);
+  const int64_t base = sell_base(A, i);
   const int len = A.row_len[i];
   const T acc = sell_row<T, T, false, LdNc, D16>(T(0), base, len, val, A, i, x);
   if (mode == 0) {
@@ -202,9 +249,10 @@ __global__ void __launch_bounds__(256) k_jacobi_lower(SellDev L, const T* __rest
   int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= L.n_rows) return;
   const VecIO<T, HINT> io;
-  const int64_t base = L.slice_off[i >> 5] + (i & 31);
+  const int64_t base = sell_base(L, i);
   const int len = L.row_len[i];
   T acc = io.ld(b + i);
+  // (a plain loop: measured faster here than the all-slots-at-once row)
   for (int k = 0; k < len; ++k) {
     const int64_t q = base + 32 * (int64_t)k;
     acc = rn_sub(acc, rn_mul(ldg_stream(lval + q), io.ld(x + sell_col<D16>(L, i, q))));
@@ -222,7 +270,7 @@ __global__ void __launch_bounds__(256) k_jacobi_upper(SellDev U, const T* __rest
   int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= U.n_rows) return;
   const VecIO<T, HINT> io;
-  const int64_t base = U.slice_off[i >> 5] + (i & 31);
+  const int64_t base = sell_base(U, i);
   const int len = U.row_len[i];
   T acc = io.ld(b + i);
   for (int k = 0; k < len; ++k) {
@@ -244,7 +292,7 @@ __global__ void __launch_bounds__(256) k_jacobi_lower_diag(SellDev L, const T* _
   int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= L.n_rows) return;
   const VecIO<T, HINT> io;
-  const int64_t base = L.slice_off[i >> 5] + (i & 31);
+  const int64_t base = sell_base(L, i);
   const int len = L.row_len[i];
   T f = io.ld(b + i);
   for (int k = 0; k < len; ++k) {
@@ -282,7 +330,7 @@ __global__ void __launch_bounds__(256) k_gather_jacobi_lower(SellDev L,
                                                              T* __restrict__ xn) {
   int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= L.n_rows) return;
-  const int64_t base = L.slice_off[i >> 5] + (i & 31);
+  const int64_t base = sell_base(L, i);
   const int len = L.row_len[i];
   const VecIO<T, HINT> io;
   const T bi = (T)r[gmap[i]];
@@ -352,7 +400,7 @@ __device__ __forceinline__ void jc_rows(const SellDev& M, const T* __restrict__ 
       const int32_t i = i0 + m * blockDim.x;
       const bool ok = i < hi && i >= lo;
       const int32_t ic = ok ? i : lo;
-      const int64_t base = M.slice_off[ic >> 5] + (ic & 31);
+      const int64_t base = sell_base(M, ic);
       const int len = ok ? M.row_len[ic] : 0;
       acc[m] = sell_row<T, T, true, LdCg, false>(ok ? __ldcg(b + ic) : T(0), base, len, val, M, ic, x);
     }
