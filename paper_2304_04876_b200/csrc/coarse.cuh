@@ -204,14 +204,10 @@ __global__ void __launch_bounds__(256) k_restrict_columns(int32_t n_c, const int
 // interior rows: z[g] = double( (Phi v)[g] + (0 + y_a + ...) ), Phi row =
 // dense panel row over the subdomain's sorted coarse columns (coalesced)
 template <typename T>
-__global__ void __launch_bounds__(CH_THREADS) k_prolong_interior(ChunkDev D, const T* __restrict__ panel,
-                                                                 const T* __restrict__ v,
-                                                                 const int32_t* __restrict__ sc_ptr,
-                                                                 const int32_t* __restrict__ sc_pos,
-                                                                 const T* __restrict__ y,
-                                                                 RemoteAdd RA,
-                                                                 double* __restrict__ z) {
-  const int32_t ch = blockIdx.x;
+__device__ __forceinline__ void prolong_interior_chunk(int32_t ch, const ChunkDev& D, const T* __restrict__ panel,
+                                                       const T* __restrict__ v, const int32_t* __restrict__ sc_ptr,
+                                                       const int32_t* __restrict__ sc_pos, const T* __restrict__ y,
+                                                       const RemoteAdd& RA, double* __restrict__ z) {
   if (threadIdx.x >= D.chunk_nrow[ch]) return;
   const int32_t s = D.chunk_sub[ch];
   const int32_t ni = D.n_int[s];
@@ -227,25 +223,43 @@ __global__ void __launch_bounds__(CH_THREADS) k_prolong_interior(ChunkDev D, con
 }
 
 // interface rows: Phi_Gamma row (CSR by interface position) + scatter
+struct ProlongGamma {
+  int32_t n_gamma;
+  const int32_t* gamma_rows;
+  const int64_t* pg_ptr;
+  const int32_t* pg_col;
+};
+
 template <typename T>
-__global__ void __launch_bounds__(256) k_prolong_interface(int32_t n_gamma, const int32_t* __restrict__ gamma_rows,
-                                                           const int64_t* __restrict__ pg_ptr,
-                                                           const int32_t* __restrict__ pg_col,
-                                                           const T* __restrict__ pg_val,
-                                                           const T* __restrict__ v,
-                                                           const int32_t* __restrict__ sc_ptr,
-                                                           const int32_t* __restrict__ sc_pos,
-                                                           const T* __restrict__ y,
-                                                           RemoteAdd RA,
-                                                           double* __restrict__ z) {
-  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n_gamma) return;
+__device__ __forceinline__ void prolong_interface_row(int32_t t, const ProlongGamma& G, const T* __restrict__ pg_val,
+                                                      const T* __restrict__ v, const int32_t* __restrict__ sc_ptr,
+                                                      const int32_t* __restrict__ sc_pos, const T* __restrict__ y,
+                                                      const RemoteAdd& RA, double* __restrict__ z) {
+  if (t >= G.n_gamma) return;
+  const int32_t* gamma_rows = G.gamma_rows;
+  const int64_t* pg_ptr = G.pg_ptr;
+  const int32_t* pg_col = G.pg_col;
   const int32_t g = gamma_rows[t];
   T zc = T(0);
   for (int64_t p = pg_ptr[t]; p < pg_ptr[t + 1]; ++p) zc = rn_add(zc, rn_mul(pg_val[p], v[pg_col[p]]));
   T acc = RA.start<T>(g);
   for (int32_t q = sc_ptr[g]; q < sc_ptr[g + 1]; ++q) acc = rn_add(acc, y[sc_pos[q]]);
   z[g] = (double)rn_add(zc, RA.finish<T>(g, acc));
+}
+
+// the whole prolongation + scatter in one launch: CTAs [0, n_chunks) take
+// interior chunks (panel rows), the rest take interface rows
+template <typename T>
+__global__ void __launch_bounds__(CH_THREADS) k_prolong(int32_t n_chunks, ChunkDev D, const T* __restrict__ panel,
+                                                        ProlongGamma G, const T* __restrict__ pg_val,
+                                                        const T* __restrict__ v, const int32_t* __restrict__ sc_ptr,
+                                                        const int32_t* __restrict__ sc_pos, const T* __restrict__ y,
+                                                        RemoteAdd RA, double* __restrict__ z) {
+  if ((int32_t)blockIdx.x < n_chunks)
+    prolong_interior_chunk<T>(blockIdx.x, D, panel, v, sc_ptr, sc_pos, y, RA, z);
+  else
+    prolong_interface_row<T>((blockIdx.x - n_chunks) * CH_THREADS + threadIdx.x, G, pg_val, v, sc_ptr, sc_pos, y,
+                             RA, z);
 }
 
 // dense replicated coarse solve: v = A0^-1 u, one warp per row

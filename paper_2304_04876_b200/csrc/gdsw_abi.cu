@@ -581,8 +581,15 @@ struct gdsw_precond {
   DBuf<char> xb, x1, x2, x3, pdot, cu, cv;
   std::mutex mu;
   cudaEvent_t last = nullptr;
+  // side stream for the coarse restriction + solve, overlapped with the
+  // local solves (fork/join by events; single-GPU path)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   ~gdsw_precond() {
     if (last) cudaEventDestroy(last);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
     plan_release(plan);
   }
   const void* panel() const { return dtype == GDSW_F32 ? (const void*)panel32.p : (const void*)panel64.p; }
@@ -1005,20 +1012,30 @@ void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
     ProfScope ps("halo_fwd", s, 0.0);
     Dd->halo_fwd(const_cast<double*>(r), s);
   }
+  // the coarse restriction and solve only read r: on one GPU they run on
+  // the side stream, overlapped with the local solves, joined before the
+  // prolongation
+  const bool fork = Cp && !Dd && !env_flag("GDSW_NO_OVERLAP");
+  cudaStream_t cs = s;
+  if (fork) {
+    CK(cudaEventRecord(m->ev_fork, s));
+    CK(cudaStreamWaitEvent(m->side, m->ev_fork, 0));
+    cs = m->side;
+  }
   if (Cp) {
     ChunkDev D = Cp->chunk_dev();
     if (Cp->n_chunks > 0) {
       // panels once + r at interior rows (4 B index + 8 B value)
-      ProfScope ps("restrict_panels", s, (double)Cp->panel_entries * sizeof(T) + Cp->n_int_total * 12.0);
-      k_restrict_chunks<T><<<Cp->n_chunks, CH_THREADS, 0, s>>>(D, (const T*)m->panel(), r, (T*)m->pdot.p);
+      ProfScope ps("restrict_panels", cs, (double)Cp->panel_entries * sizeof(T) + Cp->n_int_total * 12.0);
+      k_restrict_chunks<T><<<Cp->n_chunks, CH_THREADS, 0, cs>>>(D, (const T*)m->panel(), r, (T*)m->pdot.p);
       CK_LAUNCH();
     }
     {
-      ProfScope ps("restrict_columns", s, (double)Cp->h_pgt_val.size() * (sizeof(T) + 12) +
-                                              (double)Cp->n_cpart * (sizeof(T) + 8));
-      k_restrict_columns<T><<<Cp->n_c, 256, 0, s>>>(Cp->n_c, Cp->pgt_ptr.p, Cp->pgt_row.p,
-                                                    (const T*)m->pgt_val.p, r, Cp->cpart_ptr.p,
-                                                    Cp->cpart_idx.p, (const T*)m->pdot.p, (T*)m->cu.p);
+      ProfScope ps("restrict_columns", cs, (double)Cp->h_pgt_val.size() * (sizeof(T) + 12) +
+                                               (double)Cp->n_cpart * (sizeof(T) + 8));
+      k_restrict_columns<T><<<Cp->n_c, 256, 0, cs>>>(Cp->n_c, Cp->pgt_ptr.p, Cp->pgt_row.p,
+                                                     (const T*)m->pgt_val.p, r, Cp->cpart_ptr.p,
+                                                     Cp->cpart_idx.p, (const T*)m->pdot.p, (T*)m->cu.p);
       CK_LAUNCH();
     }
     if (Dd) {
@@ -1030,11 +1047,12 @@ void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
       k_cast_from_f64<T><<<grid_for(Cp->n_c, TB), TB, 0, s>>>(Cp->n_c, m->red64.p + Cp->n_c, (T*)m->cu.p);
       CK_LAUNCH();
     }
-    ProfScope ps("coarse_solve", s, (double)Cp->n_c * Cp->n_c * sizeof(T));
-    k_coarse_gemv<T><<<grid_for(Cp->n_c, TB / 32), TB, 0, s>>>(Cp->n_c, (const T*)m->ainv.p,
-                                                               (const T*)m->cu.p, (T*)m->cv.p);
+    ProfScope ps("coarse_solve", cs, (double)Cp->n_c * Cp->n_c * sizeof(T));
+    k_coarse_gemv<T><<<grid_for(Cp->n_c, TB / 32), TB, 0, cs>>>(Cp->n_c, (const T*)m->ainv.p,
+                                                                (const T*)m->cu.p, (T*)m->cv.p);
     CK_LAUNCH();
   }
+  if (fork) CK(cudaEventRecord(m->ev_join, m->side));
   T* y = local_solve<T>(m, r, 0, s);
   RemoteAdd RA{};
   int64_t own_lo = 0, own_hi = P->n;
@@ -1055,24 +1073,23 @@ void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
     own_lo = Dd->own_off;
     own_hi = Dd->own_off + Dd->n_own;
   }
+  if (fork) CK(cudaStreamWaitEvent(s, m->ev_join, 0));
   if (Cp) {
+    // interior rows (panel row dot, coalesced) and interface rows (CSR
+    // Phi_Gamma), each + its local contributions, in one launch
     ChunkDev D = Cp->chunk_dev();
-    // interior rows: panel row dot (coalesced) + their local contributions
-    if (Cp->n_chunks > 0) {
-      ProfScope ps("prolong_interior", s, (double)Cp->panel_entries * sizeof(T) +
-                                              Cp->n_int_total * (4.0 + 8.0 + 8.0 + 4.0 + sizeof(T)));
-      k_prolong_interior<T><<<Cp->n_chunks, CH_THREADS, 0, s>>>(D, (const T*)m->panel(), (const T*)m->cv.p,
-                                                               P->sc_ptr.p, P->sc_pos.p, y, RA, z);
-      CK_LAUNCH();
-    }
     const double ng = (double)Cp->n_gamma;
-    ProfScope ps("prolong_interface", s, (double)Cp->h_pgr_val.size() * (sizeof(T) + 4) +
-                                             ng * (4.0 + 8.0 + 8.0 + 8.0) +
-                                             (double)(P->n_loc - Cp->n_int_total) * (4.0 + sizeof(T)));
-    if (Cp->n_gamma > 0) {
-      k_prolong_interface<T><<<grid_for(Cp->n_gamma, TB), TB, 0, s>>>(
-          (int32_t)Cp->n_gamma, Cp->gamma32.p, Cp->pgam_ptr.p, Cp->pgam_col.p, (const T*)m->pgr_val.p,
-          (const T*)m->cv.p, P->sc_ptr.p, P->sc_pos.p, y, RA, z);
+    ProfScope ps("prolong", s, (double)Cp->panel_entries * sizeof(T) +
+                                   Cp->n_int_total * (4.0 + 8.0 + 8.0 + 4.0 + sizeof(T)) +
+                                   (double)Cp->h_pgr_val.size() * (sizeof(T) + 4) + ng * (4.0 + 8.0 + 8.0 + 8.0) +
+                                   (double)(P->n_loc - Cp->n_int_total) * (4.0 + sizeof(T)));
+    const int32_t nblk = Cp->n_chunks + (int32_t)((Cp->n_gamma + CH_THREADS - 1) / CH_THREADS);
+    if (nblk > 0) {
+      k_prolong<T><<<nblk, CH_THREADS, 0, s>>>(Cp->n_chunks, D, (const T*)m->panel(),
+                                               ProlongGamma{(int32_t)Cp->n_gamma, Cp->gamma32.p, Cp->pgam_ptr.p,
+                                                            Cp->pgam_col.p},
+                                               (const T*)m->pgr_val.p, (const T*)m->cv.p, P->sc_ptr.p, P->sc_pos.p,
+                                               y, RA, z);
       CK_LAUNCH();
     }
   } else {
@@ -1122,6 +1139,9 @@ int gdsw_precond_create(gdsw_precond** out, gdsw_plan* plan, int dtype, int tris
     m->x2.alloc(nl);
     m->x3.alloc(nl);
     CK(cudaEventCreateWithFlags(&m->last, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&m->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
     CK(cudaEventRecord(m->last, 0));
     *out = m.release();
   });
