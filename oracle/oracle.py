@@ -249,6 +249,11 @@ class OracleSchwarz:
         self.symbolics = symbolics
         self.method = spec.method
         self.iters = spec.trisolve_iters
+        # apply: subdomain solves on a thread pool like the reference's
+        # `threads` option (schwarz.py:111-127, 310-324); the C kernels run
+        # without the GIL, the sum stays in subdomain order
+        self.threads = max(1, threads)
+        self._pool = ThreadPoolExecutor(max_workers=self.threads) if self.threads > 1 else None
 
         def one(i):
             blk = extract_submatrix(local_src, self.sets[i], self.sets[i])
@@ -284,8 +289,13 @@ class OracleSchwarz:
             v = levelset_solve(a0_sym, a0_l, a0_u, u)
             zc = csr_spmv(phi, v)
         z = np.zeros(self.n, dtype=rw.dtype)
-        for i, dofs in enumerate(self.sets):
-            z[dofs] += self.local_solve(i, rw[dofs])
+        if self._pool is not None:
+            ys = list(self._pool.map(lambda i: self.local_solve(i, rw[self.sets[i]]),
+                                     range(len(self.sets))))
+        else:
+            ys = (self.local_solve(i, rw[dofs]) for i, dofs in enumerate(self.sets))
+        for dofs, y in zip(self.sets, ys):
+            z[dofs] += y
         if zc is not None:
             z = zc + z
         return z.astype(np.float64) if self.single else z
