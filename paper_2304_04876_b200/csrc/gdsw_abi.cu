@@ -630,7 +630,7 @@ struct gdsw_precond {
     if (!stream_built) {
       TriStream::Fac L{&P->h_l_ptr, &P->h_l_idx, &P->h_llev_sub, &P->h_llev_ptr, &P->h_llev_rows, 0};
       TriStream::Fac U{&P->h_u_ptr, &P->h_u_idx, &P->h_ulev_sub, &P->h_ulev_ptr, &P->h_ulev_rows, 1};
-      tstream.build(P->n_sub, P->h_sub_ptr, L, U, (int)es);
+      tstream.build(P->n_sub, P->h_sub_ptr, L, U, (int)es, P->method != GDSW_EXACT_LU);
       stream_built = true;
     }
     with_dtype(dtype, [&](auto tag) {

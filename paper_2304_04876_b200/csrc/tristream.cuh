@@ -38,6 +38,9 @@ constexpr int TR_SHORT = 32;
 constexpr int TR_SEG = 128;
 constexpr int TR_MAXW = 64;                     // warp tasks per chunk
 constexpr int TR_CHUNK_MIN = 16 * 1024;
+constexpr int TR_SN_MIN = 32;                   // rows of a supernode worth a dense block
+constexpr int TR_SN_HDR = 48;                   // header bytes of a supernode chunk
+enum TrChunkType : int { TR_ROWS = 0, TR_SN_GEMV = 1, TR_SN_DIAG = 2, TR_SN_UPD = 3 };
 
 __host__ __device__ inline int64_t ts_al16(int64_t b) { return (b + 15) & ~int64_t(15); }
 
@@ -88,7 +91,10 @@ struct TriStream {
     int skip;  // 1: U (diagonal first, stored separately)
   };
 
-  void build(int32_t n_sub, const std::vector<int64_t>& sub_ptr, const Fac& L, const Fac& U, int vsize_) {
+  // bitwise: medium rows keep the reference's sequential subtraction order
+  // (ILU(k)); exact factors use a shuffle tree there (compared at 1e-13)
+  void build(int32_t n_sub, const std::vector<int64_t>& sub_ptr, const Fac& L, const Fac& U, int vsize_,
+             bool bitwise) {
     vsize = vsize_;
     const int64_t nnz_l = L.ptr->back();
     max_rows = 0;
@@ -110,6 +116,7 @@ struct TriStream {
     std::vector<int64_t> h_ch_off, p_src, p_dst;
     std::vector<int32_t> p_len, p_stride;
 
+    struct SN { int64_t a, k, m; };
     // one chunk under construction
     struct WT { int32_t row, len, first, nseg; int64_t src; int64_t diag_src; };
     struct SL { std::vector<int32_t> rows, lens; std::vector<int64_t> srcs, dsrc; int32_t width; };
@@ -132,7 +139,7 @@ struct TriStream {
       auto put32 = [&](int64_t at, int32_t v) { std::memcpy(c + at, &v, 4); };
       put32(0, nw);
       put32(4, nsl);
-      put32(8, up ? 1 : 0);
+      put32(8, (up ? 1 : 0) | (bitwise ? 2 : 0));
       int64_t dp = cl.data;
       const std::vector<int64_t>& idx = *(up ? U.idx : L.idx);
       auto put_cols = [&](int64_t at, int64_t src, int32_t n, int32_t stride) {
@@ -208,16 +215,190 @@ struct TriStream {
       data_bytes = 0;
     };
 
+    // supernode [a, a+k) with external pattern of m columns, solved in
+    // order q = 0..k-1 over rows a + q (L) or a + k - 1 - q (U):
+    //  GEMV chunks  x[row_q] -= V_q . x[E]           (rows [q0, q0+nq), row-major)
+    //  DIAG chunk   32-row diagonal tile, one warp    (tile column-major 32x32)
+    //  UPD chunks   x[row_q] -= P_q . x[block]       (rows below, panel column-major)
+    auto emit_sn = [&](const SN& sn, int64_t base, const std::vector<int64_t>& ptr,
+                       const std::vector<int64_t>& idx, int skip) {
+      flush();
+      const bool U = skip == 1;
+      const int64_t k = sn.k, m = sn.m, V = vsize;
+      const int32_t brow = (int32_t)(U ? sn.a + k - 1 : sn.a), dir = U ? -1 : 1;
+      const int64_t uoff = U ? nnz_l : 0;
+      auto grow = [&](int64_t q) { return base + (U ? sn.a + k - 1 - q : sn.a + q); };
+      // src position of the entry of row q on triangle column q' (< q)
+      auto tri_src = [&](int64_t q, int64_t qp) {
+        const int64_t g = grow(q);
+        return U ? ptr[g] + (q - qp) : ptr[g] + m + qp;
+      };
+      auto new_chunk = [&](int64_t bytes, int type, const int32_t* h1, const int32_t* h2) {
+        const int64_t off = (int64_t)buf.size();
+        const int64_t len = ts_al16(bytes);
+        require(len <= chunk_max, "internal: supernode chunk overflow");
+        buf.resize(off + len, 0);
+        unsigned char* c = buf.data() + off;
+        const int32_t h0[4] = {0, 0, U ? 1 : 0, type};
+        std::memcpy(c, h0, 16);
+        std::memcpy(c + 16, h1, 16);
+        std::memcpy(c + 32, h2, 16);
+        h_ch_off.push_back(off);
+        h_ch_len.push_back((int32_t)len);
+        return off;
+      };
+      auto place = [&](int64_t src, int64_t dst_byte, int32_t len, int32_t stride) {
+        if (len <= 0) return;
+        p_src.push_back(src);
+        p_dst.push_back(dst_byte / V);
+        p_len.push_back(len);
+        p_stride.push_back(stride);
+      };
+      // GEMV over the external pattern
+      if (m > 0) {
+        const int64_t eb = ts_al16(m * csize);
+        const int64_t nq_max = std::max<int64_t>(1, (chunk_max - TR_SN_HDR - eb) / (m * V));
+        require(TR_SN_HDR + eb + m * V <= chunk_max, "supernode pattern too wide for a chunk");
+        for (int64_t q0 = 0; q0 < k; q0 += nq_max) {
+          const int64_t nq = std::min(nq_max, k - q0);
+          const int32_t h1[4] = {brow, dir, (int32_t)q0, (int32_t)nq};
+          const int32_t h2[4] = {(int32_t)m, TR_SN_HDR, (int32_t)(TR_SN_HDR + eb), 0};
+          const int64_t off = new_chunk(TR_SN_HDR + eb + nq * m * V, TR_SN_GEMV, h1, h2);
+          unsigned char* c = buf.data() + off;
+          // E = the external columns of the first-solved row
+          const int64_t g0 = grow(0);
+          for (int64_t p = 0; p < m; ++p) {
+            const int64_t col = idx[ptr[g0] + skip + p];
+            if (csize == 2) {
+              const uint16_t h = (uint16_t)col;
+              std::memcpy(c + TR_SN_HDR + 2 * p, &h, 2);
+            } else {
+              const int32_t h = (int32_t)col;
+              std::memcpy(c + TR_SN_HDR + 4 * p, &h, 4);
+            }
+          }
+          for (int64_t q = q0; q < q0 + nq; ++q) {
+            const int64_t g = grow(q);
+            const int64_t src = U ? ptr[g] + 1 + q : ptr[g];
+            place(uoff + src, off + TR_SN_HDR + eb + (q - q0) * m * V, (int32_t)m, 1);
+          }
+        }
+      }
+      // dense triangle, 32-row blocks
+      for (int64_t jb = 0; jb < k; jb += 32) {
+        const int64_t nb = std::min<int64_t>(32, k - jb);
+        {
+          const int32_t h1[4] = {brow, dir, (int32_t)jb, (int32_t)nb};
+          const int32_t h2[4] = {TR_SN_HDR, U ? (int32_t)(TR_SN_HDR + 32 * 32 * V) : 0, 0, 0};
+          const int64_t off = new_chunk(TR_SN_HDR + 32 * 32 * V + (U ? 32 * V : 0), TR_SN_DIAG, h1, h2);
+          for (int64_t l = 0; l < nb; ++l) {
+            const int64_t q = jb + l;
+            if (l > 0) {
+              if (!U) place(tri_src(q, jb), off + TR_SN_HDR + l * V, (int32_t)l, 32);
+              else place(uoff + tri_src(q, q - 1), off + TR_SN_HDR + ((l - 1) * 32 + l) * V, (int32_t)l, -32);
+            }
+            if (U) place(uoff + ptr[grow(q)], off + TR_SN_HDR + 32 * 32 * V + l * V, 1, 1);
+          }
+        }
+        const int64_t rest = k - jb - nb;
+        if (rest <= 0) continue;
+        const int64_t nq_max = std::max<int64_t>(1, (chunk_max - TR_SN_HDR) / (nb * V));
+        for (int64_t q0 = jb + nb; q0 < k; q0 += nq_max) {
+          const int64_t nq = std::min(nq_max, k - q0);
+          const int32_t h1[4] = {brow, dir, (int32_t)jb, (int32_t)nb};
+          const int32_t h2[4] = {(int32_t)q0, (int32_t)nq, TR_SN_HDR, 0};
+          const int64_t off = new_chunk(TR_SN_HDR + nb * nq * V, TR_SN_UPD, h1, h2);
+          for (int64_t q = q0; q < q0 + nq; ++q) {
+            if (!U) place(tri_src(q, jb), off + TR_SN_HDR + (q - q0) * V, (int32_t)nb, (int32_t)nq);
+            else
+              place(uoff + tri_src(q, jb + nb - 1), off + TR_SN_HDR + ((nb - 1) * nq + (q - q0)) * V, (int32_t)nb,
+                    -(int32_t)nq);
+          }
+        }
+      }
+    };
+
     for (int32_t s = 0; s < n_sub; ++s) {
       h_ch_sub[s] = (int32_t)h_ch_off.size();
       const int64_t base = sub_ptr[s];
       for (const Fac* f : {&L, &U}) {
         up = f->skip == 1;
         const std::vector<int64_t>& ptr = *f->ptr;
-        for (int64_t lv = (*f->lsub)[s]; lv < (*f->lsub)[s + 1]; ++lv) {
+        const int64_t n_s = sub_ptr[s + 1] - base;
+        const std::vector<int64_t>& idx = *f->idx;
+        auto rlen = [&](int64_t i) { return ptr[base + i + 1] - ptr[base + i] - f->skip; };
+        auto rcol = [&](int64_t i, int64_t k) { return idx[ptr[base + i] + f->skip + k]; };
+        // supernodes: runs of rows whose patterns nest by one (dense diagonal
+        // block, shared external pattern); L: row i = row i-1 + {i-1};
+        // U: row i = {i+1} + row i+1
+        std::vector<SN> sns;
+        std::vector<int32_t> sn_of(n_s, -1);
+        {
+          auto nests = [&](int64_t i, int64_t prev) {  // row i extends row prev by one
+            const int64_t li = rlen(i), lp = rlen(prev);
+            if (li != lp + 1) return false;
+            if (!up) {
+              if (rcol(i, li - 1) != prev) return false;
+              for (int64_t k = 0; k < lp; ++k)
+                if (rcol(i, k) != rcol(prev, k)) return false;
+            } else {
+              if (rcol(i, 0) != prev) return false;
+              for (int64_t k = 0; k < lp; ++k)
+                if (rcol(i, k + 1) != rcol(prev, k)) return false;
+            }
+            return true;
+          };
+          int64_t i = 0;
+          while (i < n_s) {
+            int64_t j = i + 1;
+            if (!up) {
+              while (j < n_s && nests(j, j - 1)) ++j;
+            } else {
+              while (j < n_s && nests(j - 1, j)) ++j;
+            }
+            if (!bitwise && j - i >= TR_SN_MIN) {
+              SN sn{i, j - i, up ? rlen(j - 1) : rlen(i)};
+              for (int64_t r = i; r < j; ++r) sn_of[r] = (int32_t)sns.size();
+              sns.push_back(sn);
+            }
+            i = j;
+          }
+        }
+        // unit levels (a supernode is one unit)
+        std::vector<int32_t> lev(n_s, 0);
+        int32_t nlev = 0;
+        auto unit_level = [&](int64_t i) {
+          int32_t lv = 0;
+          for (int64_t k = 0, l = rlen(i); k < l; ++k) {
+            const int64_t c = rcol(i, k);
+            if (sn_of[i] >= 0 && sn_of[c] == sn_of[i]) continue;
+            lv = std::max(lv, lev[c] + 1);
+          }
+          return lv;
+        };
+        for (int64_t t = 0; t < n_s; ++t) {
+          const int64_t i = up ? n_s - 1 - t : t;
+          const int32_t q = sn_of[i];
+          if (q >= 0 && i != (up ? sns[q].a + sns[q].k - 1 : sns[q].a)) {
+            lev[i] = lev[up ? sns[q].a + sns[q].k - 1 : sns[q].a];
+            continue;
+          }
+          lev[i] = unit_level(i);
+          nlev = std::max(nlev, lev[i] + 1);
+        }
+        std::vector<std::vector<int64_t>> lrows_of(nlev);
+        std::vector<std::vector<int32_t>> lsn_of(nlev);
+        for (int64_t t = 0; t < n_s; ++t) {
+          const int64_t i = up ? n_s - 1 - t : t;
+          const int32_t q = sn_of[i];
+          if (q < 0) lrows_of[lev[i]].push_back(i);
+          else if (i == (up ? sns[q].a + sns[q].k - 1 : sns[q].a)) lsn_of[lev[i]].push_back(q);
+        }
+        for (int32_t lv = 0; lv < nlev; ++lv) {
+          for (int32_t q : lsn_of[lv]) emit_sn(sns[q], base, ptr, idx, f->skip);
           std::vector<int64_t> shorts;
-          for (int64_t t = (*f->lptr)[lv]; t < (*f->lptr)[lv + 1]; ++t) {
-            const int64_t row = (*f->lrows)[t], g = base + row;
+          for (const int64_t row : lrows_of[lv]) {
+            const int64_t g = base + row;
             const int64_t len = ptr[g + 1] - ptr[g] - f->skip;
             if (len <= TR_SHORT) {
               shorts.push_back(row);
@@ -346,12 +527,68 @@ __device__ __forceinline__ void consumer_bar() {
 // ---------------------------------------------------------------------------
 // chunk solve
 // ---------------------------------------------------------------------------
+// supernode chunks (dense blocks of exact-LU separators). Rows are indexed
+// in solve order q: row(q) = brow + dir * q.
+template <typename T, typename CT>
+__device__ __forceinline__ void ts_sn_chunk(const unsigned char* __restrict__ c, int type, bool up, T* x) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int4 h1 = *reinterpret_cast<const int4*>(c + 16);
+  const int4 h2 = *reinterpret_cast<const int4*>(c + 32);
+  const int32_t brow = h1.x, dir = h1.y;
+  if (type == TR_SN_GEMV) {
+    // x[row_q] -= V_q . x[E], one warp per row, lanes over the pattern
+    const int32_t q0 = h1.z, nq = h1.w, m = h2.x;
+    const CT* E = reinterpret_cast<const CT*>(c + h2.y);
+    const T* V = reinterpret_cast<const T*>(c + h2.z);
+    for (int t = warp; t < nq; t += TR_CWARPS) {
+      const T* v = V + (int64_t)t * m;
+      T acc = T(0);
+#pragma unroll 4
+      for (int p = lane; p < m; p += 32) acc = fma(v[p], x[E[p]], acc);
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        const int32_t row = brow + dir * (q0 + t);
+        x[row] = x[row] - acc;
+      }
+    }
+  } else if (type == TR_SN_DIAG) {
+    // 32-row diagonal tile: lane l owns row jb + l; column j is final after
+    // the updates of columns < j (U: then divided by its diagonal)
+    if (warp != 0) return;
+    const int32_t jb = h1.z, nb = h1.w;
+    const T* tile = reinterpret_cast<const T*>(c + h2.x);
+    const T* dg = up ? reinterpret_cast<const T*>(c + h2.y) : nullptr;
+    const int32_t row = brow + dir * (jb + lane);
+    T t = lane < nb ? x[row] : T(0);
+    for (int j = 0; j < nb; ++j) {
+      if (up && lane == j) t = t / dg[j];
+      const T xj = __shfl_sync(0xffffffffu, t, j);
+      if (lane > j && lane < nb) t = fma(-tile[j * 32 + lane], xj, t);
+    }
+    if (lane < nb) x[row] = t;
+  } else {
+    // x[row_q] -= P_q . x[block jb], thread per row, panel column-major
+    const int32_t jb = h1.z, nb = h1.w, q0 = h2.x, nq = h2.y;
+    const T* P = reinterpret_cast<const T*>(c + h2.z);
+    for (int t = threadIdx.x; t < nq; t += TR_CTHREADS) {
+      T acc = T(0);
+      for (int j = 0; j < nb; ++j) acc = fma(P[(int64_t)j * nq + t], x[brow + dir * (jb + j)], acc);
+      const int32_t row = brow + dir * (q0 + t);
+      x[row] = x[row] - acc;
+    }
+  }
+}
+
 template <typename T, typename CT>
 __device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T* x, T* part, int* cnt) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int4 hdr = *reinterpret_cast<const int4*>(c);
+  if (hdr.w != TR_ROWS) {
+    ts_sn_chunk<T, CT>(c, hdr.w, hdr.z & 1, x);
+    return;
+  }
   const int nw = hdr.x, nsl = hdr.y;
-  const bool up = hdr.z & 1;
+  const bool up = hdr.z & 1, ordered = hdr.z & 2;
   const ChunkLayout cl(nw, nsl, up, (int)sizeof(T));
   // warp tasks (medium rows and segments of long rows)
   for (int t = warp; t < nw; t += TR_CWARPS) {
@@ -366,7 +603,18 @@ __device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T*
       const int k = lane + 32 * u;
       p[u] = k < len ? rn_mul(v[k], x[cc[k]]) : T(0);
     }
-    if (gp.y == 1) {
+    if (gp.y == 1 && !ordered) {
+      // whole row in one segment, fixed tree
+      T acc = T(0);
+#pragma unroll
+      for (int u = 0; u < TR_SEG / 32; ++u) acc += p[u];
+      acc = warp_sum(acc);
+      if (lane == 0) {
+        T xi = x[row] - acc;
+        if (up) xi = rn_div(xi, reinterpret_cast<const T*>(c + cl.wdiag)[t]);
+        x[row] = xi;
+      }
+    } else if (gp.y == 1) {
       // whole row in one segment: subtraction chain in column order
       T xi = x[row];
 #pragma unroll
