@@ -926,11 +926,16 @@ T* levelset_solve(gdsw_precond* m, const double* r, cudaStream_t s) {
       const char* e = std::getenv("GDSW_TS_BUDGET_KB");
       return e ? (int64_t)std::atoi(e) * 1024 : (int64_t)0;
     }();
-    // measured on B200: a 64 KB budget beats larger rings (C1, C3-sized
-    // blocks and C2 ILU(0) all faster than at 100 or 220 KB)
-    const int64_t budget = ring_env ? ring_env : 64 * 1024;
+    // measured on B200: the iterate in shared memory beats global/L1 as
+    // soon as it fits next to a ring of >= 4 chunks (C1 1.20 -> 0.87 ms,
+    // C3-sized blocks 2.11 -> 1.67 ms per solve); prefer a budget that keeps
+    // two CTAs per SM; an iterate in global memory wants a mid-size ring
+    // (L1 left for its gathers: C2 ILU(0) 0.71 -> 0.60 ms)
     const int64_t xs = ts.max_rows * (int64_t)sizeof(T);
-    const bool smx = budget - xs >= 4LL * ts.chunk_max;
+    const int64_t need = xs + 4LL * ts.chunk_max;
+    int64_t budget = need <= 110 * 1024 ? 110 * 1024 : (need <= 220 * 1024 ? 220 * 1024 : 160 * 1024);
+    if (ring_env) budget = ring_env;
+    const bool smx = budget - xs >= 4LL * ts.chunk_max && !env_flag("GDSW_TS_XGLOBAL");
     const int64_t ring = std::max<int64_t>(2LL * ts.chunk_max, ((smx ? budget - xs : budget) & ~int64_t(15)));
     const size_t smem = (size_t)ring + (smx ? (size_t)xs : 0);
     require(smem <= 220 * 1024, "streamed SpTRSV chunk too large");

@@ -108,6 +108,38 @@ def test_local_solves_bitwise_against_oracle(name):
 
 
 @pytest.mark.parametrize("name", [n for n in sorted(CASES) if CASES[n][4] == "fast_ilu"])
+def test_fastsptrsv_dataflow_and_apply_overlap_variants(name):
+    """The opt-in dataflow FastSpTRSV (one persistent launch) is bit-identical
+    to the per-sweep launches; the apply with and without the side-stream
+    coarse overlap is bit-identical too."""
+    import os
+    torch = _torch()
+    prob, dec, cfg, skel, pre = setup_case(name)
+    r = torch.from_numpy(probes(prob.a.nrows, ks=(5,))[0]).cuda()
+    dt = torch.float32 if cfg.precision == "single" else torch.float64
+    n_loc = skel._local_plan["n_loc"]
+    y0 = torch.empty(n_loc, dtype=dt, device="cuda")
+    pre._dev.local_solve(r, y0)
+    try:
+        os.environ["GDSW_JACOBI_FLOW"] = "1"
+        for _ in range(3):   # several launches: epochs and tickets carry over
+            y1 = torch.full((n_loc,), float("nan"), dtype=dt, device="cuda")
+            pre._dev.local_solve(r, y1)
+            assert torch.equal(y0, y1)
+    finally:
+        del os.environ["GDSW_JACOBI_FLOW"]
+    z0 = torch.empty_like(r)
+    pre._dev.apply(r, z0)
+    try:
+        os.environ["GDSW_NO_OVERLAP"] = "1"
+        z1 = torch.empty_like(r)
+        pre._dev.apply(r, z1)
+    finally:
+        del os.environ["GDSW_NO_OVERLAP"]
+    assert torch.equal(z0, z1)
+
+
+@pytest.mark.parametrize("name", [n for n in sorted(CASES) if CASES[n][4] == "fast_ilu"])
 def test_fastilu_factors_bitwise_against_oracle(name):
     prob, dec, cfg, skel, pre = setup_case(name)
     ore = O.OracleSchwarz(prob.a, dec, cfg, prob.nullspace if cfg.use_coarse else None,
