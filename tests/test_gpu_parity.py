@@ -107,6 +107,29 @@ def test_local_solves_bitwise_against_oracle(name):
             assert np.abs(got - want).max() <= LONG_ROW_TOL * np.abs(want).max(), f"subdomain {i}"
 
 
+@pytest.mark.parametrize("method,fill", [("ilu_k", 0), ("ilu_k", 2)])
+def test_large_block_streamed_sptrsv_bitwise(method, fill):
+    """A single block larger than 65,536 rows: 32-bit block columns in the
+    stream and the iterate in global memory (the C2-like layout of the
+    streamed SpTRSV); ILU(k) rows stay bit-identical to the oracle."""
+    torch = _torch()
+    prob = mp.assemble_laplace3d(mp.Grid3D(42, 42, 40))
+    dec = dd.decompose(prob.a, dd.box_partition(prob.grid, 1, 1, 1), 1, None)
+    cfg = sw.SchwarzConfig(local=ls.SolverSpec(method, fill), use_coarse=False,
+                           ordering="natural")
+    skel = sw.setup_symbolic(prob.a, dec, cfg)
+    pre = sw.setup_numeric(skel, prob.a, None)
+    assert skel.sets[0].size > 65536
+    ore = O.OracleSchwarz(prob.a, dec, cfg, None, symbolics=skel.local_symbolics)
+    r = probes(prob.a.nrows, ks=(3,))[0]
+    y = torch.empty(skel._local_plan["n_loc"], dtype=torch.float64, device="cuda")
+    pre._dev.local_solve(torch.from_numpy(r).cuda(), y)
+    want = ore.local_solve(0, r[skel.sets[0]])
+    got = np.empty_like(want)
+    got[skel.local_symbolics[0].ordering.perm] = y.cpu().numpy()
+    assert np.array_equal(got, want)
+
+
 @pytest.mark.parametrize("name", [n for n in sorted(CASES) if CASES[n][4] == "fast_ilu"])
 def test_fastsptrsv_dataflow_and_apply_overlap_variants(name):
     """The opt-in dataflow FastSpTRSV (one persistent launch) is bit-identical
