@@ -20,7 +20,7 @@ from paper_2304_04876_b200.model_problems import (Grid3D, assemble_elasticity3d,
 from paper_2304_04876_b200.schwarz import SchwarzConfig, setup_numeric, setup_symbolic  # noqa: E402
 
 CONFIGS = {
-    # name: (kind, n, boxes, solver, ordering, precision)
+    # name: (kind, n, boxes (p or (px, py, pz)), solver, ordering, precision[, coarse])
     "C1": ("laplace", 30, 2, SolverSpec("exact_lu"), "nested_dissection", "double"),
     "C2": ("laplace", 128, 4, SolverSpec("fast_ilu", 0, 3, 5), "natural", "double"),
     "C2ilu": ("laplace", 128, 4, SolverSpec("ilu_k", 0), "natural", "double"),
@@ -29,22 +29,30 @@ CONFIGS = {
     "C4": ("laplace", 200, 5, SolverSpec("fast_ilu", 0, 3, 5), "natural", "single"),
     "C4double": ("laplace", 200, 5, SolverSpec("fast_ilu", 0, 3, 5), "natural", "double"),
     "C5_512": ("laplace", 128, 8, SolverSpec("fast_ilu", 0, 3, 5), "natural", "double"),
+    # the paper's subdomains-per-GPU study at 2M dof (128^3), fast_ilu(0,3,5)
+    "C5_1": ("laplace", 128, 1, SolverSpec("fast_ilu", 0, 3, 5), "natural", "double", None),
+    "C5_8": ("laplace", 128, 2, SolverSpec("fast_ilu", 0, 3, 5), "natural", "double"),
+    "C5_64": ("laplace", 128, 4, SolverSpec("fast_ilu", 0, 3, 5), "natural", "double"),
+    "C5_216": ("laplace", 128, 6, SolverSpec("fast_ilu", 0, 3, 5), "natural", "double"),
+    "C5_256": ("laplace", 128, (8, 8, 4), SolverSpec("fast_ilu", 0, 3, 5), "natural", "double"),
 }
 
 
 def run(name):
-    kind, n, p, spec, ordk, prec = CONFIGS[name]
+    kind, n, p, spec, ordk, prec, *rest = CONFIGS[name]
+    coarse = rest[0] if rest else "rgdsw"
+    px, py, pz = p if isinstance(p, tuple) else (p, p, p)
     t0 = time.perf_counter()
     grid = Grid3D(n, n, n)
     prob = assemble_laplace3d(grid) if kind == "laplace" else assemble_elasticity3d(grid)
-    dec = decompose(prob.a, box_partition(prob.grid, p, p, p), 1, "rgdsw")
+    dec = decompose(prob.a, box_partition(prob.grid, px, py, pz), 1, coarse)
     t_in = time.perf_counter() - t0
-    cfg = SchwarzConfig(local=spec, ordering=ordk, precision=prec)
+    cfg = SchwarzConfig(local=spec, ordering=ordk, precision=prec, use_coarse=coarse is not None)
     t0 = time.perf_counter()
     skel = setup_symbolic(prob.a, dec, cfg)
     t_sym = time.perf_counter() - t0
     t0 = time.perf_counter()
-    pre = setup_numeric(skel, prob.a, prob.nullspace)
+    pre = setup_numeric(skel, prob.a, prob.nullspace if coarse else None)
     torch.cuda.synchronize()
     t_num = time.perf_counter() - t0
     x_star = np.random.default_rng(0).standard_normal(prob.a.nrows)
@@ -59,7 +67,7 @@ def run(name):
     e1.record()
     torch.cuda.synchronize()
     xh = x.cpu().numpy()
-    out = dict(config=name, n=prob.a.nrows, subdomains=p ** 3,
+    out = dict(config=name, n=prob.a.nrows, subdomains=px * py * pz,
                n_coarse=pre.coarse.a0.nrows if pre.coarse else 0,
                setup_s=dict(inputs=t_in, symbolic=t_sym, numeric=t_num),
                iterations=rep.iterations, converged=rep.converged,
