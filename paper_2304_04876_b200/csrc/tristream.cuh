@@ -20,9 +20,10 @@
 //  * medium rows (<= TR_SEG entries): one warp per row, products in
 //    parallel, subtraction chain in column order (bit-identical);
 //  * long rows: TR_SEG-entry segments, one warp each, fused products and a
-//    fixed shuffle tree; the last segment to finish (smem counter) combines
+//    fixed shuffle tree; after a barrier the first segment's thread combines
 //    the partials in segment order -- deterministic, within 1e-13 relative
-//    of sequential substitution.
+//    of sequential substitution (exact factors use the tree for medium rows
+//    too; ILU(k) keeps the sequential chain).
 #pragma once
 #include <algorithm>
 #include <cstring>
@@ -139,7 +140,9 @@ struct TriStream {
       auto put32 = [&](int64_t at, int32_t v) { std::memcpy(c + at, &v, 4); };
       put32(0, nw);
       put32(4, nsl);
-      put32(8, (up ? 1 : 0) | (bitwise ? 2 : 0));
+      bool multi = false;
+      for (const WT& w : wts) multi = multi || w.nseg > 1;
+      put32(8, (up ? 1 : 0) | (bitwise ? 2 : 0) | (multi ? 4 : 0));
       int64_t dp = cl.data;
       const std::vector<int64_t>& idx = *(up ? U.idx : L.idx);
       auto put_cols = [&](int64_t at, int64_t src, int32_t n, int32_t stride) {
@@ -580,7 +583,7 @@ __device__ __forceinline__ void ts_sn_chunk(const unsigned char* __restrict__ c,
 }
 
 template <typename T, typename CT>
-__device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T* x, T* part, int* cnt) {
+__device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T* x, T* part) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int4 hdr = *reinterpret_cast<const int4*>(c);
   if (hdr.w != TR_ROWS) {
@@ -633,19 +636,7 @@ __device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T*
 #pragma unroll
       for (int u = 0; u < TR_SEG / 32; ++u) acc += p[u];
       acc = warp_sum(acc);
-      if (lane == 0) {
-        part[t] = acc;
-        __threadfence_block();
-        if (atomicAdd(cnt + gp.x, 1) == gp.y - 1) {
-          __threadfence_block();
-          T s = T(0);
-          for (int q = 0; q < gp.y; ++q) s += *(volatile T*)(part + gp.x + q);
-          T xi = x[row] - s;
-          if (up) xi = rn_div(xi, reinterpret_cast<const T*>(c + cl.wdiag)[gp.x]);
-          x[row] = xi;
-          cnt[gp.x] = 0;
-        }
-      }
+      if (lane == 0) part[t] = acc;  // combined after the barrier below
     }
   }
   // short rows: one thread each, sequential in column order
@@ -675,6 +666,21 @@ __device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T*
     if (up) acc = rn_div(acc, reinterpret_cast<const T*>(c + cl.sdiag)[t]);
     x[row] = acc;
   }
+  if (hdr.z & 4) {
+    // rows split in segments: partials summed in segment order by the
+    // thread of the first segment once every segment is in
+    consumer_bar();
+    for (int t = threadIdx.x; t < nw; t += TR_CTHREADS) {
+      const int2 gp = *reinterpret_cast<const int2*>(c + cl.wgrp + 8 * t);
+      if (gp.y < 2 || gp.x != t) continue;
+      const int32_t row = reinterpret_cast<const int4*>(c + cl.wtab)[t].x;
+      T sum = T(0);
+      for (int q = 0; q < gp.y; ++q) sum += part[t + q];
+      T xi = x[row] - sum;
+      if (up) xi = rn_div(xi, reinterpret_cast<const T*>(c + cl.wdiag)[t]);
+      x[row] = xi;
+    }
+  }
 }
 
 // one CTA per subdomain: gather (ordering folded into gmap), every chunk of
@@ -692,7 +698,6 @@ __global__ void __launch_bounds__(TR_THREADS_ALL) k_trisolve_stream(TriStreamDev
   __shared__ uint64_t full[TR_NT], empty[TR_NT];
   __shared__ int32_t pos[TR_NT], foot[TR_NT];
   __shared__ T part[TR_MAXW];
-  __shared__ int cnt[TR_MAXW];
   const int s = blockIdx.x;
   const int32_t base = sub_ptr[s], ns = sub_ptr[s + 1] - base;
   const int c0 = S.ch_sub[s], c1 = S.ch_sub[s + 1];
@@ -706,7 +711,6 @@ __global__ void __launch_bounds__(TR_THREADS_ALL) k_trisolve_stream(TriStreamDev
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (threadIdx.x < TR_MAXW) cnt[threadIdx.x] = 0;
   __syncthreads();
   if (threadIdx.x >= TR_CTHREADS) {
     // producer warp: the chunk table is read 32 entries at a time, one
@@ -756,7 +760,7 @@ __global__ void __launch_bounds__(TR_THREADS_ALL) k_trisolve_stream(TriStreamDev
   for (int i = 0; i < nch; ++i) {
     const int t = i % TR_NT;
     mbar_wait(&full[t], (uint32_t)((i / TR_NT) & 1));
-    ts_chunk<T, CT>(ring + pos[t], x, part, cnt);
+    ts_chunk<T, CT>(ring + pos[t], x, part);
     consumer_bar();
     if (threadIdx.x == 0) mbar_arrive(&empty[t]);
   }
