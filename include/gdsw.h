@@ -123,6 +123,12 @@ typedef struct {
 } gdsw_coarse_desc;
 
 int gdsw_plan_create(gdsw_plan** out, const gdsw_local_desc* local);
+/* permuted block pattern of A for the GPU numeric LU (exact_lu / ilu_k):
+ * ab_ptr[n_loc+1] over the concatenated permuted block rows, ab_idx the
+ * block-local column, ab_src the A.values position of each entry
+ * (permute_symmetric + extract_submatrix, local_solvers.py:306-327) */
+int gdsw_plan_set_block_pattern(gdsw_plan* p, const int64_t* ab_ptr, const int64_t* ab_idx,
+                                const int64_t* ab_src);
 int gdsw_plan_destroy(gdsw_plan* p);
 
 /* ------------------------------------------------------------------------
@@ -141,6 +147,11 @@ int gdsw_precond_set_factors(gdsw_precond* m, const void* l_vals, const void* u_
  * residuals[sweep * n_sub + s] receives the per-sweep nonlinear residuals */
 int gdsw_precond_fastilu(gdsw_precond* m, const gdsw_csr* a, int sweeps, double* residuals);
 int gdsw_precond_get_factors(const gdsw_precond* m, void* l_vals, void* u_vals);
+/* IKJ numeric LU / ILU(k) of every block on the GPU, bit-exact with the
+ * reference (lu_numeric, _kernels.py:429-466; local_solvers.py:306-340);
+ * a = the f64 operator (values cast to the precond dtype); fail_rows[n_sub]
+ * gets 1 + the first row whose pivot is <= 1e-14 ||A_s||_inf, or 0 */
+int gdsw_precond_lu_numeric(gdsw_precond* m, const gdsw_csr* a, double diag_shift, int64_t* fail_rows);
 /* harmonic extension on the GPU (harmonic_extension, coarse_space.py:130-179);
  * a = the f64 operator the coarse basis is built from; col_resid[K] gets the
  * max |A_II phi_I + A_IG phi_G| per panel column */

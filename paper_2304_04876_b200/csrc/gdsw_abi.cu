@@ -22,6 +22,7 @@
 #include "trisolve.cuh"
 #include "tristream.cuh"
 #include "jacobi_flow.cuh"
+#include "lu_numeric.cuh"
 
 using namespace gdsw;
 
@@ -193,6 +194,15 @@ struct gdsw_plan {
   std::vector<int64_t> h_llev_sub, h_llev_ptr, h_llev_rows, h_ulev_sub, h_ulev_ptr, h_ulev_rows;
   TriSched l_sched, u_sched;     // exact / ILU(k) level-set layouts
   bool sched_ready = false;
+  // numeric LU on the GPU: permuted block pattern of A + device schedules
+  bool has_ab = false;
+  int32_t n_max = 0;
+  DBuf<int64_t> ab_ptr, ab_src;
+  DBuf<int32_t> ab_idx, l_idx32, u_idx32, lu_lev_sub, lu_lev_ptr, lu_lev_rows;
+  LuDev lu_dev() const {
+    return LuDev{sub_ptr.p, l_ptr.p, l_idx32.p, u_ptr.p, u_idx32.p, lu_lev_sub.p, lu_lev_ptr.p,
+                 lu_lev_rows.p, ab_ptr.p, ab_idx.p, ab_src.p, n_max};
+  }
   std::vector<int64_t> row_add;  // block row offset per concatenated row
   std::vector<int64_t> h_l_idx, h_u_idx;
   SellPattern l_sell, u_sell;    // Jacobi layouts (U without its diagonal)
@@ -1193,6 +1203,63 @@ int gdsw_precond_get_factors(const gdsw_precond* m, void* l_vals, void* u_vals) 
     gdsw_plan* P = m->plan;
     if (P->nnz_l) CK(cudaMemcpy(l_vals, m->lval.p, P->nnz_l * m->es, cudaMemcpyDeviceToHost));
     if (P->nnz_u) CK(cudaMemcpy(u_vals, m->uval.p, P->nnz_u * m->es, cudaMemcpyDeviceToHost));
+  });
+}
+
+int gdsw_plan_set_block_pattern(gdsw_plan* P, const int64_t* ab_ptr, const int64_t* ab_idx,
+                                const int64_t* ab_src) {
+  return guarded([&] {
+    const int64_t nab = ab_ptr[P->n_loc];
+    P->ab_ptr.upload(vec(ab_ptr, P->n_loc + 1));
+    P->ab_idx.upload(to_i32(ab_idx, nab));
+    P->ab_src.upload(vec(ab_src, nab));
+    P->l_idx32.upload(to_i32(P->h_l_idx.data(), P->h_l_idx.size()));
+    P->u_idx32.upload(to_i32(P->h_u_idx.data(), P->h_u_idx.size()));
+    P->lu_lev_sub.upload(to_i32(P->h_llev_sub.data(), P->h_llev_sub.size()));
+    P->lu_lev_ptr.upload(to_i32(P->h_llev_ptr.data(), P->h_llev_ptr.size()));
+    P->lu_lev_rows.upload(to_i32(P->h_llev_rows.data(), P->h_llev_rows.size()));
+    int64_t mx = 0;
+    for (int32_t s = 0; s < P->n_sub; ++s) mx = std::max<int64_t>(mx, P->h_sub_ptr[s + 1] - P->h_sub_ptr[s]);
+    P->n_max = (int32_t)mx;
+    P->has_ab = true;
+  });
+}
+
+int gdsw_precond_lu_numeric(gdsw_precond* m, const gdsw_csr* a, double diag_shift, int64_t* fail_rows) {
+  return guarded([&] {
+    gdsw_plan* P = m->plan;
+    require(P->has_ab, "plan has no block pattern for the numeric LU");
+    require(a->dtype == GDSW_F64, "the numeric LU reads the float64 operator values");
+    const double* av = (const double*)a->csr_val.p;
+    DBuf<double> norm(std::max(P->n_sub, 1));
+    DBuf<int64_t> fail(std::max(P->n_sub, 1));
+    std::vector<int64_t> none(std::max(P->n_sub, 1), INT64_MAX);
+    CK(cudaMemcpy(fail.p, none.data(), none.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    with_dtype(m->dtype, [&](auto tag) {
+      using T = decltype(tag);
+      const size_t nscr = (size_t)P->n_sub * LU_WARPS * std::max(P->n_max, 1);
+      DBuf<T> w(nscr);
+      DBuf<int32_t> stamp(nscr);
+      CK(cudaMemset(stamp.p, 0xff, nscr * sizeof(int32_t)));
+      if (P->nnz_l) CK(cudaMemset(m->lval.p, 0, P->nnz_l * sizeof(T)));
+      if (P->nnz_u) CK(cudaMemset(m->uval.p, 0, P->nnz_u * sizeof(T)));
+      const LuDev D = P->lu_dev();
+      k_block_norm_inf<T><<<P->n_sub, LU_THREADS>>>(D, av, norm.p);
+      CK_LAUNCH();
+      k_lu_numeric<T><<<P->n_sub, LU_THREADS>>>(D, av, (T)diag_shift, norm.p, (T*)m->lval.p, (T*)m->uval.p,
+                                                w.p, stamp.p, fail.p);
+      CK_LAUNCH();
+      CK(cudaDeviceSynchronize());
+    });
+    std::vector<int64_t> f = fail.download();
+    for (int32_t s = 0; s < P->n_sub; ++s) fail_rows[s] = f[s] == INT64_MAX ? 0 : f[s];
+    m->has_factors = true;
+    m->jacobi_ready = false;
+    m->sched_vals_ready = false;
+    m->stream_vals_ready = false;
+    if (P->method == GDSW_FAST_ILU) m->ensure_jacobi();
+    else if (env_flag("GDSW_TS_SCHED")) m->ensure_sched_vals();
+    else m->ensure_stream_vals();
   });
 }
 

@@ -63,6 +63,8 @@ _SIGS = {
     "gdsw_precond_set_factors": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "gdsw_precond_fastilu": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     "gdsw_precond_get_factors": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gdsw_plan_set_block_pattern": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gdsw_precond_lu_numeric": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p]),
     "gdsw_precond_extend": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_void_p,
                                       C.c_void_p]),
     "gdsw_precond_panel_entries": (C.c_int64, [C.c_void_p]),
@@ -240,6 +242,10 @@ class Plan:
         self.n_sub = local["n_sub"]
         self.nnz_l = int(local["l_ptr"][-1])
         self.nnz_u = int(local["u_ptr"][-1])
+        self.has_block_pattern = local.get("ab_ptr") is not None
+        if self.has_block_pattern:
+            ab = [_i64(local[k]) for k in ("ab_ptr", "ab_idx", "ab_src")]
+            _ck(_lib.gdsw_plan_set_block_pattern(h, *[_ptr(x) for x in ab]))
 
     def __del__(self):
         h = getattr(self, "handle", None)
@@ -283,6 +289,13 @@ class Precond:
         res = np.zeros((sweeps, n_sub), dtype=np.float64)
         _ck(_lib.gdsw_precond_fastilu(self.handle, a_dev.handle, int(sweeps), _ptr(res)))
         return res
+
+    def lu_numeric(self, a_dev: DeviceCsr, diag_shift: float, n_sub: int) -> np.ndarray:
+        """GPU IKJ factorization of every block; returns 1 + the first failing
+        row per block (0 = ok)."""
+        fail = np.zeros(max(n_sub, 1), dtype=np.int64)
+        _ck(_lib.gdsw_precond_lu_numeric(self.handle, a_dev.handle, float(diag_shift), _ptr(fail)))
+        return fail[:n_sub]
 
     def factors(self, nnz_l: int, nnz_u: int):
         lv = np.empty(nnz_l, dtype=self.value_dtype)

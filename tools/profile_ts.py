@@ -32,7 +32,21 @@ def main():
     dec = decompose(prob.a, box_partition(prob.grid, p, p, p), 1, "rgdsw")
     cfg = SchwarzConfig(local=spec, ordering=ordk, use_coarse=False)
     skel = setup_symbolic(prob.a, dec, cfg)
+    import os
+    import time
+    os.environ["GDSW_HOST_LU"] = "1"
+    t0 = time.perf_counter()
+    setup_numeric(skel, prob.a, None)
+    t_host = time.perf_counter() - t0
+    os.environ["GDSW_HOST_LU"] = "0"
+    setup_numeric(skel, prob.a, None)   # warm-up (schedules, streams)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
     pre = setup_numeric(skel, prob.a, None)
+    torch.cuda.synchronize()
+    t_gpu = time.perf_counter() - t0
+    del os.environ["GDSW_HOST_LU"]
+    print(f"{name}: numeric setup host IKJ {t_host:.3f} s, GPU {t_gpu:.3f} s", flush=True)
     nloc = skel._local_plan["n_loc"]
     r = torch.from_numpy(np.random.default_rng(1).standard_normal(prob.a.nrows)).cuda()
     y = torch.empty(nloc, dtype=torch.float64, device="cuda")
