@@ -159,6 +159,10 @@ int gdsw_precond_extend(gdsw_precond* m, const gdsw_csr* a, double tol, int max_
                         int* iters_out, double* col_resid);
 int64_t gdsw_precond_panel_entries(const gdsw_precond* m);
 int gdsw_precond_get_panels(const gdsw_precond* m, double* panels);
+/* Galerkin product A0 = Phi^T A Phi on the GPU (coarse_matrix,
+ * coarse_space.py:205-207) from the extension's float64 panels: column c =
+ * restriction of A (Phi e_c); a0_dense gets n_c x n_c row-major float64 */
+int gdsw_precond_coarse_galerkin(gdsw_precond* m, const gdsw_csr* a, double* a0_dense);
 /* dense A0^-1 (n_c x n_c, row-major, float64; cast to the precond dtype) */
 int gdsw_precond_set_coarse_inverse(gdsw_precond* m, const double* a0inv);
 /* z = Phi A0^-1 Phi^T r + sum_i R_i^T A_i^-1 R_i r  (apply, schwarz.py:290-327) */

@@ -236,9 +236,11 @@ def reproduction_coefficients(column_map, n_nullspace: int, coeffs=None) -> np.n
     return c
 
 
-def extend_on_device(pre, a_dev, a: CsrMatrix, structure, basis, sets):
+def extend_on_device(pre, a_dev, a: CsrMatrix, structure, basis, sets, lazy_phi: bool = False):
     """Bind the coarse structure to a device preconditioner, run the batched
-    extension, check it, and return (phi, column_map, desc)."""
+    extension, check it, and return (phi, column_map, desc); with lazy_phi,
+    phi is a thunk assembling the host CsrMatrix on demand (the solve path
+    only uses the device panels)."""
     column_map, pg = coarse_columns(structure, basis)
     if not column_map:
         raise ValueError("coarse space is empty; use use_coarse=False")
@@ -247,6 +249,8 @@ def extend_on_device(pre, a_dev, a: CsrMatrix, structure, basis, sets):
     _, col_resid = pre.extend(a_dev, int(desc["col_ptr"][-1]), EXTENSION_TOL,
                               EXTENSION_MAX_ITERS)
     check_extension_residual(a, desc, pg, col_resid)
+    if lazy_phi:
+        return (lambda: assemble_phi(structure.n, desc, pg, pre.panels())), column_map, desc
     phi = assemble_phi(structure.n, desc, pg, pre.panels())
     return phi, column_map, desc
 

@@ -1444,6 +1444,59 @@ int gdsw_precond_get_panels(const gdsw_precond* m, double* panels) {
   });
 }
 
+// e_c as a coarse vector
+__global__ void k_unit(int32_t n, int32_t c, double* __restrict__ v) {
+  const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i == c ? 1.0 : 0.0;
+}
+
+int gdsw_precond_coarse_galerkin(gdsw_precond* m, const gdsw_csr* a, double* a0_dense) {
+  return guarded([&] {
+    require(m->cp != nullptr && m->has_phi, "coarse basis is not set up");
+    require(a->dtype == GDSW_F64, "the Galerkin product reads the float64 operator values");
+    CoarsePlan* Cp = m->cp.get();
+    gdsw_plan* P = m->plan;
+    const int32_t nc = Cp->n_c;
+    const int64_t n = P->n;
+    // float64 Phi: panels (always kept in f64) + interface values
+    DBuf<double> pgr(std::max<size_t>(Cp->h_pgr_val.size(), 1)), pgt(std::max<size_t>(Cp->h_pgt_val.size(), 1));
+    if (!Cp->h_pgr_val.empty()) CK(cudaMemcpy(pgr.p, Cp->h_pgr_val.data(), Cp->h_pgr_val.size() * 8, cudaMemcpyHostToDevice));
+    if (!Cp->h_pgt_val.empty()) CK(cudaMemcpy(pgt.p, Cp->h_pgt_val.data(), Cp->h_pgt_val.size() * 8, cudaMemcpyHostToDevice));
+    DBuf<double> v(std::max(nc, 1)), z(std::max<int64_t>(n, 1)), y(std::max<int64_t>(n, 1)),
+        zero_loc(std::max<int64_t>(P->n_loc, 1)), part(std::max<int64_t>(Cp->n_partial, 1)),
+        a0((size_t)std::max(nc, 1) * std::max(nc, 1));
+    zero_loc.zero();
+    const ChunkDev D = Cp->chunk_dev();
+    const int32_t nblk = Cp->n_chunks + (int32_t)((Cp->n_gamma + CH_THREADS - 1) / CH_THREADS);
+    // column c of A0 = Phi^T (A (Phi e_c)): the apply's own prolongation,
+    // SpMV and restriction kernels in float64
+    for (int32_t c = 0; c < nc; ++c) {
+      k_unit<<<grid_for(nc, TB), TB>>>(nc, c, v.p);
+      CK_LAUNCH();
+      if (nblk > 0) {
+        k_prolong<double><<<nblk, CH_THREADS>>>(Cp->n_chunks, D, m->panel64.p,
+                                               ProlongGamma{(int32_t)Cp->n_gamma, Cp->gamma32.p, Cp->pgam_ptr.p,
+                                                            Cp->pgam_col.p},
+                                               pgr.p, v.p, P->sc_ptr.p, P->sc_pos.p, zero_loc.p, RemoteAdd{}, z.p);
+        CK_LAUNCH();
+      }
+      spmv_T<double>(a, z.p, nullptr, y.p, 0, 1.0, 0.0, 0);
+      if (Cp->n_chunks > 0) {
+        k_restrict_chunks<double><<<Cp->n_chunks, CH_THREADS>>>(D, m->panel64.p, y.p, part.p);
+        CK_LAUNCH();
+      }
+      k_restrict_columns<double><<<nc, 256>>>(nc, Cp->pgt_ptr.p, Cp->pgt_row.p, pgt.p, y.p, Cp->cpart_ptr.p,
+                                              Cp->cpart_idx.p, part.p, a0.p + (size_t)c * nc);
+      CK_LAUNCH();
+    }
+    CK(cudaDeviceSynchronize());
+    // a0 holds columns contiguously: transpose into the row-major output
+    std::vector<double> h = a0.download();
+    for (int32_t c = 0; c < nc; ++c)
+      for (int32_t r = 0; r < nc; ++r) a0_dense[(size_t)r * nc + c] = h[(size_t)c * nc + r];
+  });
+}
+
 int gdsw_precond_set_coarse_inverse(gdsw_precond* m, const double* a0inv) {
   return guarded([&] {
     require(m->cp != nullptr, "preconditioner has no coarse structure");

@@ -65,6 +65,7 @@ _SIGS = {
     "gdsw_precond_get_factors": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "gdsw_plan_set_block_pattern": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "gdsw_precond_lu_numeric": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p]),
+    "gdsw_precond_coarse_galerkin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "gdsw_precond_extend": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_void_p,
                                       C.c_void_p]),
     "gdsw_precond_panel_entries": (C.c_int64, [C.c_void_p]),
@@ -296,6 +297,12 @@ class Precond:
         fail = np.zeros(max(n_sub, 1), dtype=np.int64)
         _ck(_lib.gdsw_precond_lu_numeric(self.handle, a_dev.handle, float(diag_shift), _ptr(fail)))
         return fail[:n_sub]
+
+    def coarse_galerkin(self, a_dev: DeviceCsr, n_c: int) -> np.ndarray:
+        """Dense A0 = Phi^T A Phi (float64) from the device coarse basis."""
+        out = np.zeros((n_c, n_c), dtype=np.float64)
+        _ck(_lib.gdsw_precond_coarse_galerkin(self.handle, a_dev.handle, _ptr(out)))
+        return out
 
     def factors(self, nnz_l: int, nnz_u: int):
         lv = np.empty(nnz_l, dtype=self.value_dtype)

@@ -28,7 +28,6 @@ import numpy as np
 
 from . import _host
 from .coarse_space import (
-    coarse_matrix,
     extend_on_device,
     interface_basis,
     interior_sets as _interior_sets,
@@ -283,13 +282,29 @@ class PreconditionerSkeleton:
         return self._device_plan
 
 
-@dataclass
 class CoarseSolver:
-    phi: CsrMatrix
-    phi_t: CsrMatrix
-    a0: CsrMatrix
-    a0_factorization: LocalFactorization
-    column_map: list
+    """Coarse operator pieces (schwarz.py:84-99). `phi` may be given as a
+    thunk: the solve path uses the device panels, the host CsrMatrix of Phi
+    (and its transpose) is assembled on first access."""
+
+    def __init__(self, phi, phi_t, a0: CsrMatrix, a0_factorization: LocalFactorization,
+                 column_map: list):
+        self._phi, self._phi_t = phi, phi_t
+        self.a0 = a0
+        self.a0_factorization = a0_factorization
+        self.column_map = column_map
+
+    @property
+    def phi(self) -> CsrMatrix:
+        if callable(self._phi):
+            self._phi = self._phi()
+        return self._phi
+
+    @property
+    def phi_t(self) -> CsrMatrix:
+        if self._phi_t is None:
+            self._phi_t = transpose(self.phi)
+        return self._phi_t
 
 
 class TwoLevelPreconditioner:
@@ -465,18 +480,22 @@ def setup_numeric(skeleton: PreconditionerSkeleton, a: CsrMatrix,
             raise ValueError("two-level numeric setup needs the operator null space columns")
         structure = skeleton.decomposition.structure
         basis = interface_basis(nullspace, structure)
-        phi, column_map, _ = extend_on_device(pre, a_src_dev, coarse_src, structure, basis,
-                                              skeleton.interior_sets)
-        a0 = coarse_matrix(coarse_src, phi)
+        phi64, column_map, _ = extend_on_device(pre, a_src_dev, coarse_src, structure, basis,
+                                                skeleton.interior_sets, lazy_phi=True)
+        # A0 = Phi^T A Phi on the GPU from the float64 panels (the reference's
+        # coarse_matrix, coarse_space.py:205-207; exact zeros of the dense
+        # product are not kept as entries)
+        a0 = CsrMatrix.from_dense(pre.coarse_galerkin(a_src_dev, len(column_map)))
+        phi = phi64
         if single:
-            phi = convert_precision(phi, np.float32)
+            phi = lambda: convert_precision(phi64(), np.float32)  # noqa: E731
             a0 = convert_precision(a0, np.float32)
         try:
             a0_fac = numeric_lu(a0, symbolic_lu(a0, make_ordering(a0, config.ordering)))
         except np.linalg.LinAlgError as err:
             raise np.linalg.LinAlgError(f"coarse matrix is singular: {err}") from err
         pre.set_coarse_inverse(np.linalg.inv(a0.to_dense().astype(np.float64)))
-        coarse = CoarseSolver(phi, transpose(phi), a0, a0_fac, column_map)
+        coarse = CoarseSolver(phi, None, a0, a0_fac, column_map)
 
     m = TwoLevelPreconditioner(skeleton.n, skeleton.sets, facs, coarse, config.precision,
                                config.threads, skeleton, pre)
