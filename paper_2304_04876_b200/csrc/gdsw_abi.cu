@@ -815,7 +815,7 @@ T* jacobi_flow_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s
   return Gf;
 }
 
-template <typename T, bool HINT, bool D16>
+template <typename T, bool HINT, bool D16, bool UNI>
 T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   gdsw_plan* P = m->plan;
   const int32_t n = (int32_t)P->n_loc;
@@ -854,14 +854,14 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   } else {
     {
       ProfScope ps("gather_jacobi_lower", s, lbytes + n * (12.0 - sizeof(T)));
-      k_gather_jacobi_lower<T, HINT, D16><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, P->gmap.p, r, B, X1);
+      k_gather_jacobi_lower<T, HINT, D16, UNI><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, P->gmap.p, r, B, X1);
       CK_LAUNCH();
     }
     T* cur = X1;
     T* oth = X2;
     for (int t = 2; t < iters - 1; ++t) {
       ProfScope ps("jacobi_lower", s, lbytes);
-      k_jacobi_lower<T, HINT, D16><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth);
+      k_jacobi_lower<T, HINT, D16, UNI><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth);
       CK_LAUNCH();
       std::swap(cur, oth);
     }
@@ -870,7 +870,7 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
       T* X3 = (T*)m->x3.p;
       {
         ProfScope ps("jacobi_lower_diag", s, lbytes + n * 2.0 * sizeof(T));
-        k_jacobi_lower_diag<T, HINT, D16><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth,
+        k_jacobi_lower_diag<T, HINT, D16, UNI><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth,
                                                 (const T*)m->udiag.p, X3);
         CK_LAUNCH();
       }
@@ -879,7 +879,7 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
       T* Hf = cur;  // B and cur are free now
       for (int t = 1; t < iters; ++t) {
         ProfScope ps("jacobi_upper", s, ubytes + n * (double)sizeof(T));
-        k_jacobi_upper<T, HINT, D16><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, Gf, Hf);
+        k_jacobi_upper<T, HINT, D16, UNI><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, Gf, Hf);
         CK_LAUNCH();
         std::swap(Gf, Hf);
       }
@@ -899,7 +899,7 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   T* oth = H;
   for (int t = 1; t < iters; ++t) {
     ProfScope ps("jacobi_upper", s, ubytes + n * (double)sizeof(T));
-    k_jacobi_upper<T, HINT, D16><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, cur, oth);
+    k_jacobi_upper<T, HINT, D16, UNI><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, cur, oth);
     CK_LAUNCH();
     std::swap(cur, oth);
   }
@@ -941,11 +941,15 @@ T* levelset_solve(gdsw_precond* m, const double* r, cudaStream_t s) {
     // C3-sized blocks 2.11 -> 1.67 ms per solve); prefer a budget that keeps
     // two CTAs per SM; an iterate in global memory wants a mid-size ring
     // (L1 left for its gathers: C2 ILU(0) 0.71 -> 0.60 ms)
+    static const int64_t min_chunks = [] {
+      const char* e = std::getenv("GDSW_TS_MINCHUNKS");
+      return e ? (int64_t)std::atoi(e) : (int64_t)4;
+    }();
     const int64_t xs = ts.max_rows * (int64_t)sizeof(T);
-    const int64_t need = xs + 4LL * ts.chunk_max;
+    const int64_t need = xs + min_chunks * ts.chunk_max;
     int64_t budget = need <= 110 * 1024 ? 110 * 1024 : (need <= 220 * 1024 ? 220 * 1024 : 160 * 1024);
     if (ring_env) budget = ring_env;
-    const bool smx = budget - xs >= 4LL * ts.chunk_max && !env_flag("GDSW_TS_XGLOBAL");
+    const bool smx = budget - xs >= min_chunks * ts.chunk_max && !env_flag("GDSW_TS_XGLOBAL");
     const int64_t ring = std::max<int64_t>(2LL * ts.chunk_max, ((smx ? budget - xs : budget) & ~int64_t(15)));
     const size_t smem = (size_t)ring + (smx ? (size_t)xs : 0);
     require(smem <= 220 * 1024, "streamed SpTRSV chunk too large");
@@ -1010,9 +1014,19 @@ T* local_solve(gdsw_precond* m, const double* r, int jacobi_iters, cudaStream_t 
         return d16 ? jacobi_flow_solve<T, true, 4>(m, r, it, s) : jacobi_flow_solve<T, false, 4>(m, r, it, s);
       return d16 ? jacobi_flow_solve<T, true, 2>(m, r, it, s) : jacobi_flow_solve<T, false, 2>(m, r, it, s);
     }
+    // uniform-width rows (all slots loaded at once): C2 sweeps 28.0/35.2/33.9
+    // -> 25.9/30.2/27.8 us (GDSW_JACOBI_UNI=0 selects the plain loop)
+    static const bool uni_off = [] {
+      const char* e = std::getenv("GDSW_JACOBI_UNI");
+      return e && e[0] == '0';
+    }();
+    const bool uni = !uni_off && P->l_sell.uw >= 1 && P->l_sell.uw <= 4 && P->u_sell.uw >= 1 &&
+                     P->u_sell.uw <= 4;
     if (l2_hints_enabled())
-      return d16 ? jacobi_solve<T, true, true>(m, r, it, s) : jacobi_solve<T, true, false>(m, r, it, s);
-    return d16 ? jacobi_solve<T, false, true>(m, r, it, s) : jacobi_solve<T, false, false>(m, r, it, s);
+      return d16 ? jacobi_solve<T, true, true, false>(m, r, it, s) : jacobi_solve<T, true, false, false>(m, r, it, s);
+    if (uni)
+      return d16 ? jacobi_solve<T, false, true, true>(m, r, it, s) : jacobi_solve<T, false, false, true>(m, r, it, s);
+    return d16 ? jacobi_solve<T, false, true, false>(m, r, it, s) : jacobi_solve<T, false, false, false>(m, r, it, s);
   }
   return levelset_solve<T>(m, r, s);
 }

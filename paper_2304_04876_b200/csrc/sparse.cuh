@@ -241,7 +241,39 @@ struct VecIO {
   }
 };
 
-template <typename T, bool HINT, bool D16>
+// one Jacobi row: acc - sum_k val_k x[col_k] in column order. UNI (uniform
+// slice width <= 4): every slot's column and value are loaded at once,
+// independent of the row length, then the row's own gathers.
+template <typename T, bool D16, bool UNI, typename IO>
+__device__ __forceinline__ T jac_row(const SellDev& M, const T* __restrict__ val, int32_t i, int64_t base,
+                                     int len, T acc, const T* x, const IO& io) {
+  if (UNI) {
+    int32_t c[4];
+    T v[4], xv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < M.uw) {
+        const int64_t q = base + 32 * (int64_t)k;
+        c[k] = sell_col<D16>(M, i, q);
+        v[k] = ldg_stream(val + q);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < len) xv[k] = io.ld(x + c[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < len) acc = rn_sub(acc, rn_mul(v[k], xv[k]));
+    return acc;
+  }
+  for (int k = 0; k < len; ++k) {
+    const int64_t q = base + 32 * (int64_t)k;
+    acc = rn_sub(acc, rn_mul(ldg_stream(val + q), io.ld(x + sell_col<D16>(M, i, q))));
+  }
+  return acc;
+}
+
+template <typename T, bool HINT, bool D16, bool UNI>
 __global__ void __launch_bounds__(256) k_jacobi_lower(SellDev L, const T* __restrict__ lval,
                                                       const T* __restrict__ b,
                                                       const T* __restrict__ x,
@@ -251,17 +283,12 @@ __global__ void __launch_bounds__(256) k_jacobi_lower(SellDev L, const T* __rest
   const VecIO<T, HINT> io;
   const int64_t base = sell_base(L, i);
   const int len = L.row_len[i];
-  T acc = io.ld(b + i);
-  // (a plain loop: measured faster here than the all-slots-at-once row)
-  for (int k = 0; k < len; ++k) {
-    const int64_t q = base + 32 * (int64_t)k;
-    acc = rn_sub(acc, rn_mul(ldg_stream(lval + q), io.ld(x + sell_col<D16>(L, i, q))));
-  }
+  const T acc = jac_row<T, D16, UNI>(L, lval, i, base, len, io.ld(b + i), x, io);
   io.st(xn + i, acc);
 }
 
 // x_new = D^-1 (b - (U - D) x)  (U off-diagonal part in SELL, D separate)
-template <typename T, bool HINT, bool D16>
+template <typename T, bool HINT, bool D16, bool UNI>
 __global__ void __launch_bounds__(256) k_jacobi_upper(SellDev U, const T* __restrict__ uval,
                                                       const T* __restrict__ diag,
                                                       const T* __restrict__ b,
@@ -272,17 +299,13 @@ __global__ void __launch_bounds__(256) k_jacobi_upper(SellDev U, const T* __rest
   const VecIO<T, HINT> io;
   const int64_t base = sell_base(U, i);
   const int len = U.row_len[i];
-  T acc = io.ld(b + i);
-  for (int k = 0; k < len; ++k) {
-    const int64_t q = base + 32 * (int64_t)k;
-    acc = rn_sub(acc, rn_mul(ldg_stream(uval + q), io.ld(x + sell_col<D16>(U, i, q))));
-  }
+  const T acc = jac_row<T, D16, UNI>(U, uval, i, base, len, io.ld(b + i), x, io);
   io.st(xn + i, rn_div(acc, io.ld(diag + i)));
 }
 
 // last L sweep fused with the first U iterate: writes both the L result F
 // and y1 = F / diag (saves one pass over the vectors)
-template <typename T, bool HINT, bool D16>
+template <typename T, bool HINT, bool D16, bool UNI>
 __global__ void __launch_bounds__(256) k_jacobi_lower_diag(SellDev L, const T* __restrict__ lval,
                                                            const T* __restrict__ b,
                                                            const T* __restrict__ x,
@@ -294,11 +317,7 @@ __global__ void __launch_bounds__(256) k_jacobi_lower_diag(SellDev L, const T* _
   const VecIO<T, HINT> io;
   const int64_t base = sell_base(L, i);
   const int len = L.row_len[i];
-  T f = io.ld(b + i);
-  for (int k = 0; k < len; ++k) {
-    const int64_t q = base + 32 * (int64_t)k;
-    f = rn_sub(f, rn_mul(ldg_stream(lval + q), io.ld(x + sell_col<D16>(L, i, q))));
-  }
+  const T f = jac_row<T, D16, UNI>(L, lval, i, base, len, io.ld(b + i), x, io);
   io.st(xn + i, f);
   io.st(y1 + i, rn_div(f, io.ld(diag + i)));
 }
@@ -321,7 +340,7 @@ __global__ void k_gather(int32_t n, const int32_t* __restrict__ gmap, const doub
 
 // gather fused with the first Jacobi L sweep: writes b = T(r[gmap]) and the
 // second iterate b - (L - I) b in one pass over L
-template <typename T, bool HINT, bool D16>
+template <typename T, bool HINT, bool D16, bool UNI>
 __global__ void __launch_bounds__(256) k_gather_jacobi_lower(SellDev L,
                                                              const T* __restrict__ lval,
                                                              const int32_t* __restrict__ gmap,
@@ -337,23 +356,25 @@ __global__ void __launch_bounds__(256) k_gather_jacobi_lower(SellDev L,
   io.st(b + i, bi);
   // x1 = b: neighbours' b read straight from r through gmap
   T acc = bi;
-  for (int k0 = 0; k0 < len; k0 += SELL_U) {
-    int32_t c[SELL_U];
-    T v[SELL_U];
+  constexpr int W = UNI ? 4 : SELL_U;
+  const int kend = UNI ? 1 : len;  // UNI: one batch covers every slot
+  for (int k0 = 0; k0 < kend; k0 += W) {
+    int32_t c[W];
+    T v[W];
 #pragma unroll
-    for (int u = 0; u < SELL_U; ++u) {
-      if (k0 + u < len) {
+    for (int u = 0; u < W; ++u) {
+      if (UNI ? u < L.uw : k0 + u < len) {
         const int64_t q = base + 32 * (int64_t)(k0 + u);
         c[u] = sell_col<D16>(L, i, q);
         v[u] = ldg_stream(lval + q);
       }
     }
-    int32_t g[SELL_U];
+    int32_t g[W];
 #pragma unroll
-    for (int u = 0; u < SELL_U; ++u)
+    for (int u = 0; u < W; ++u)
       if (k0 + u < len) g[u] = __ldg(gmap + c[u]);
 #pragma unroll
-    for (int u = 0; u < SELL_U; ++u)
+    for (int u = 0; u < W; ++u)
       if (k0 + u < len) acc = rn_sub(acc, rn_mul(v[u], (T)__ldg(r + g[u])));
   }
   io.st(xn + i, acc);
