@@ -139,6 +139,9 @@ struct ChunkDev {
   const int32_t* col_ptr;
   const int32_t* col_ids;
   const int64_t* panel_off;
+  const int32_t* ch_g = nullptr;   // [chunk * CH_THREADS + t]: interior row
+  const int32_t* ch_y0 = nullptr;  // its first local contribution (block position) or -1
+  const int32_t* ch_ny = nullptr;  // number of local contributions
 };
 
 constexpr int CH_THREADS = 256;
@@ -157,7 +160,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_restrict_chunks(ChunkDev D, cons
   const int k = D.col_ptr[s + 1] - D.col_ptr[s];
   const bool on = threadIdx.x < D.chunk_nrow[ch];
   const int32_t row = D.chunk_row0[ch] + threadIdx.x;
-  const T rv = on ? (T)r[D.int_rows[D.int_ptr[s] + row]] : T(0);
+  const T rv = on ? (T)r[D.ch_g[(size_t)ch * CH_THREADS + threadIdx.x]] : T(0);
   const T* pc = panel + D.panel_off[s] + row;
   for (int c = 0; c < k; ++c) {
     T v = on ? ldg_stream(pc + (int64_t)c * ni) * rv : T(0);
@@ -212,13 +215,17 @@ __device__ __forceinline__ void prolong_interior_chunk(int32_t ch, const ChunkDe
   const int32_t s = D.chunk_sub[ch];
   const int32_t ni = D.n_int[s];
   const int32_t row = D.chunk_row0[ch] + threadIdx.x;
-  const int32_t g = D.int_rows[D.int_ptr[s] + row];
+  const size_t ft = (size_t)ch * CH_THREADS + threadIdx.x;
+  const int32_t g = D.ch_g[ft];
+  const int32_t y0 = D.ch_y0[ft], ny = D.ch_ny[ft];
   const T* pr = panel + D.panel_off[s] + row;
   T zc = T(0);
   for (int32_t c = D.col_ptr[s]; c < D.col_ptr[s + 1]; ++c, pr += ni)
     zc = rn_add(zc, rn_mul(ldg_stream(pr), v[D.col_ids[c]]));
   T acc = RA.start<T>(g);
-  for (int32_t q = sc_ptr[g]; q < sc_ptr[g + 1]; ++q) acc = rn_add(acc, y[sc_pos[q]]);
+  if (ny > 0) acc = rn_add(acc, y[y0]);
+  if (ny > 1)
+    for (int32_t q = sc_ptr[g] + 1; q < sc_ptr[g + 1]; ++q) acc = rn_add(acc, y[sc_pos[q]]);
   z[g] = (double)rn_add(zc, RA.finish<T>(g, acc));
 }
 

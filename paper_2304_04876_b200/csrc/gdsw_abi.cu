@@ -208,6 +208,7 @@ struct gdsw_plan {
   SellPattern l_sell, u_sell;    // Jacobi layouts (U without its diagonal)
   bool sell_ready = false;
   DBuf<int32_t> sc_ptr, sc_pos;
+  std::vector<int32_t> h_sc_ptr, h_sc_pos;
   // FastILU plan
   bool fastilu = false;
   DBuf<int64_t> a_of, fi_ptr;
@@ -254,6 +255,7 @@ struct CoarsePlan {
   int32_t n_chunks = 0;
   int64_t n_partial = 0;
   DBuf<int32_t> chunk_sub, chunk_row0, chunk_nrow, sub_chunk0;
+  DBuf<int32_t> ch_g, ch_y0, ch_ny;  // per (chunk, thread): interior row, first / number of local contributions
   DBuf<int64_t> chunk_poff;
   DBuf<int64_t> aii_ptr, aii_src, aii_diag, aig_ptr, aig_src;
   DBuf<int32_t> aii_col, aig_col;
@@ -279,8 +281,9 @@ struct CoarsePlan {
   int64_t n_cpart = 0;
   DBuf<int32_t> gamma32;
   ChunkDev chunk_dev() const {
-    return ChunkDev{chunk_sub.p, chunk_row0.p, chunk_nrow.p, chunk_poff.p, int_ptr.p,
-                    int_rows.p,  n_int.p,      col_ptr.p,    col_ids.p,    panel_off.p};
+    return ChunkDev{chunk_sub.p, chunk_row0.p, chunk_nrow.p, chunk_poff.p, int_ptr.p,  int_rows.p,
+                    n_int.p,     col_ptr.p,    col_ids.p,    panel_off.p,  ch_g.p,     ch_y0.p,
+                    ch_ny.p};
   }
   RestrictDev restrict_dev() const {
     return RestrictDev{n_c,       colsub.p,   col_ptr.p,    panel_off.p, n_int.p,
@@ -350,6 +353,8 @@ void build_local(gdsw_plan* P, const gdsw_local_desc* d) {
     for (int64_t k = 0; k < d->n_loc; ++k) pos[off[gm[k]]++] = (int32_t)k;
     P->sc_ptr.upload(cnt);
     P->sc_pos.upload(pos);
+    P->h_sc_ptr = std::move(cnt);
+    P->h_sc_pos = std::move(pos);
   }
   if (d->method == GDSW_FAST_ILU) {
     P->fastilu = true;
@@ -491,6 +496,25 @@ void build_coarse(CoarsePlan* P, const gdsw_plan* L, const gdsw_coarse_desc* c) 
     sc0[ns] = (int32_t)csub.size();
     P->n_chunks = (int32_t)csub.size();
     P->n_partial = std::max<int64_t>(poff, 1);
+    {  // flat per-thread prolongation tables: the row and its first local
+       // contribution without the int_rows -> sc_ptr -> sc_pos chain
+      const size_t nt = std::max<size_t>((size_t)P->n_chunks * CH_THREADS, 1);
+      std::vector<int32_t> fg(nt, 0), fy(nt, -1), fn(nt, 0);
+      for (int32_t ch = 0; ch < P->n_chunks; ++ch)
+        for (int32_t t = 0; t < cnrow[ch]; ++t) {
+          const int32_t s = csub[ch];
+          const int32_t g = (int32_t)irows[iptr[s] + crow0[ch] + t];
+          const size_t q = (size_t)ch * CH_THREADS + t;
+          fg[q] = g;
+          const int32_t a0 = L->h_sc_ptr.empty() ? 0 : L->h_sc_ptr[g];
+          const int32_t a1 = L->h_sc_ptr.empty() ? 0 : L->h_sc_ptr[g + 1];
+          fn[q] = a1 - a0;
+          fy[q] = a1 > a0 ? L->h_sc_pos[a0] : -1;
+        }
+      P->ch_g.upload(fg);
+      P->ch_y0.upload(fy);
+      P->ch_ny.upload(fn);
+    }
     P->chunk_sub.upload(csub);
     P->chunk_row0.upload(crow0);
     P->chunk_nrow.upload(cnrow);
