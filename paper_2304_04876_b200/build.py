@@ -36,7 +36,7 @@ def _stale(target: Path, deps) -> bool:
     return any(Path(d).stat().st_mtime > t for d in deps)
 
 
-def _deps(*dirs, suffixes=(".cu", ".cuh", ".cpp", ".h", ".hpp")):
+def _deps(*dirs, suffixes=(".cu", ".cuh", ".inc", ".cpp", ".h", ".hpp")):
     out = []
     for d in dirs:
         for p in Path(d).rglob("*"):

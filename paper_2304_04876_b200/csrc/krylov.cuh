@@ -174,7 +174,10 @@ inline void launch_block_dot(unsigned grid, cudaStream_t s, int64_t n, const dou
 
 // single-reduce update (krylov.py:346-351). coef = [a(0..j), p/delta(0..j),
 // delta, corr]. VW = 2: 16-byte vector path (rows of even ld, aligned).
-template <int VW>
+// ZM = false: the preconditioned basis Zm is not kept (zm[j] = M v[j] by
+// linearity; the cycle-end x update applies M to V y instead), so the
+// update reads V[:j], W, ZC and writes v[j], w only.
+template <int VW, bool ZM = true>
 __global__ void __launch_bounds__(256) k_sr_update(int64_t n, double* __restrict__ V,
                                                    double* __restrict__ Zm, int64_t ld, int j,
                                                    const double* __restrict__ coef,
@@ -189,45 +192,69 @@ __global__ void __launch_bounds__(256) k_sr_update(int64_t n, double* __restrict
 #pragma unroll 4
       for (int r = 0; r < j; ++r) {
         const double2 vr = ldg_stream(reinterpret_cast<const double2*>(V + r * ld + i));
-        const double2 zr = ldg_stream(reinterpret_cast<const double2*>(Zm + r * ld + i));
         const double a = __ldg(coef + r), pd = __ldg(coef + j + r);
         va.x = fma(a, vr.x, va.x);
         va.y = fma(a, vr.y, va.y);
         wp.x = fma(pd, vr.x, wp.x);
         wp.y = fma(pd, vr.y, wp.y);
-        za.x = fma(a, zr.x, za.x);
-        za.y = fma(a, zr.y, za.y);
+        if (ZM) {
+          const double2 zr = ldg_stream(reinterpret_cast<const double2*>(Zm + r * ld + i));
+          za.x = fma(a, zr.x, za.x);
+          za.y = fma(a, zr.y, za.y);
+        }
       }
       const double2 w = *reinterpret_cast<const double2*>(W + i);
-      const double2 mc = ldg_stream(reinterpret_cast<const double2*>(Mc + i));
       const double2 zc = ldg_stream(reinterpret_cast<const double2*>(Zc + i));
-      double2 vj, zj, wn;
+      double2 vj, wn;
       vj.x = (w.x - va.x) / delta;
       vj.y = (w.y - va.y) / delta;
-      zj.x = (mc.x - za.x) / delta;
-      zj.y = (mc.y - za.y) / delta;
       wn.x = zc.x / delta - wp.x - corr * vj.x;
       wn.y = zc.y / delta - wp.y - corr * vj.y;
       __stcs(reinterpret_cast<double2*>(V + (int64_t)j * ld + i), vj);
-      __stcs(reinterpret_cast<double2*>(Zm + (int64_t)j * ld + i), zj);
+      if (ZM) {
+        const double2 mc = ldg_stream(reinterpret_cast<const double2*>(Mc + i));
+        double2 zj;
+        zj.x = (mc.x - za.x) / delta;
+        zj.y = (mc.y - za.y) / delta;
+        __stcs(reinterpret_cast<double2*>(Zm + (int64_t)j * ld + i), zj);
+      }
       *reinterpret_cast<double2*>(W + i) = wn;
     } else {
       const int64_t kend = i + VW < n ? i + VW : n;
       for (int64_t k = i; k < kend; ++k) {
         double va = 0.0, wp = 0.0, za = 0.0;
         for (int r = 0; r < j; ++r) {
-          const double vr = V[r * ld + k], zr = Zm[r * ld + k];
+          const double vr = V[r * ld + k];
           va = fma(coef[r], vr, va);
           wp = fma(coef[j + r], vr, wp);
-          za = fma(coef[r], zr, za);
+          if (ZM) za = fma(coef[r], Zm[r * ld + k], za);
         }
         const double vj = (W[k] - va) / delta;
         V[(int64_t)j * ld + k] = vj;
-        Zm[(int64_t)j * ld + k] = (Mc[k] - za) / delta;
+        if (ZM) Zm[(int64_t)j * ld + k] = (Mc[k] - za) / delta;
         W[k] = Zc[k] / delta - wp - corr * vj;
       }
     }
   }
+}
+
+// t = sum_r y[r] V[r]   (the basis combination M is applied to)
+__global__ void __launch_bounds__(256) k_combine(int64_t n, const double* __restrict__ V, int64_t ld, int m,
+                                                 const double* __restrict__ y, double* __restrict__ t) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    double acc = 0.0;
+#pragma unroll 4
+    for (int r = 0; r < m; ++r) acc = fma(__ldg(y + r), ldg_stream(V + r * ld + i), acc);
+    t[i] = acc;
+  }
+}
+
+// xo = x + d
+__global__ void k_add(int64_t n, const double* __restrict__ x, const double* __restrict__ d,
+                      double* __restrict__ xo) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) xo[i] = x[i] + d[i];
 }
 
 // device-side single-reduce scalars from the fused block (krylov.py:305-306,
