@@ -264,11 +264,11 @@ __device__ __forceinline__ T jac_row(const SellDev& M, const T* __restrict__ val
 #pragma unroll
     for (int k = 0; k < 4; ++k)
       if (k < len) acc = rn_sub(acc, rn_mul(v[k], xv[k]));
-    return acc;
-  }
-  for (int k = 0; k < len; ++k) {
-    const int64_t q = base + 32 * (int64_t)k;
-    acc = rn_sub(acc, rn_mul(ldg_stream(val + q), io.ld(x + sell_col<D16>(M, i, q))));
+  } else {
+    for (int k = 0; k < len; ++k) {
+      const int64_t q = base + 32 * (int64_t)k;
+      acc = rn_sub(acc, rn_mul(ldg_stream(val + q), io.ld(x + sell_col<D16>(M, i, q))));
+    }
   }
   return acc;
 }
