@@ -617,13 +617,28 @@ struct gdsw_precond {
   cudaEvent_t last = nullptr;
   // side stream for the coarse restriction + solve, overlapped with the
   // local solves (fork/join by events; single-GPU path)
-  cudaStream_t side = nullptr;
+  cudaStream_t side = nullptr, cap = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  struct ApplyGraph {
+    const double* r;
+    double* z;
+    cudaStream_t s;
+    cudaGraphExec_t exec;
+    int64_t kernels;
+  };
+  std::vector<ApplyGraph> graphs;
+  void drop_graphs() {
+    for (auto& ag : graphs)
+      if (ag.exec) cudaGraphExecDestroy(ag.exec);
+    graphs.clear();
+  }
   ~gdsw_precond() {
+    drop_graphs();
     if (last) cudaEventDestroy(last);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (side) cudaStreamDestroy(side);
+    if (cap) cudaStreamDestroy(cap);
     plan_release(plan);
   }
   const void* panel() const { return dtype == GDSW_F32 ? (const void*)panel32.p : (const void*)panel64.p; }
@@ -1153,11 +1168,45 @@ void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
   }
 }
 
+// One apply's launches (about a dozen kernels plus the side-stream fork and
+// join) replayed as a CUDA graph: captured on the second apply with the
+// same (r, z, stream) -- the first one runs eagerly and performs every lazy
+// allocation -- and dropped whenever the preconditioner's data changes.
+// Not used while the per-kernel profiler records events, on the sharded path
+// (its collectives spin on peers) or with GDSW_NO_GRAPH=1.
+bool apply_graph_ok(const gdsw_precond* m) {
+  return !m->dist && !prof().on && !env_flag("GDSW_NO_GRAPH") && !env_flag("GDSW_NO_OVERLAP");
+}
+
 void precond_apply(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
   require(m->has_factors, "preconditioner has no numeric factors");
   if (m->cp) require(m->has_phi && m->has_ainv, "coarse space is not set up");
   std::lock_guard<std::mutex> g(m->mu);
   CK(cudaStreamWaitEvent(s, m->last, 0));
+  if (apply_graph_ok(m)) {
+    for (auto& ag : m->graphs) {
+      if (ag.r == r && ag.z == z) {
+        if (!ag.exec) {
+          // captured on a private stream (the caller's may be the legacy
+          // default stream, which cannot capture); replayed on the caller's
+          cudaGraph_t graph = nullptr;
+          const int64_t c0 = launch_counter().load();
+          CK(cudaStreamBeginCapture(m->cap, cudaStreamCaptureModeThreadLocal));
+          with_dtype(m->dtype, [&](auto tag) { apply_T<decltype(tag)>(m, r, z, m->cap); });
+          CK(cudaStreamEndCapture(m->cap, &graph));
+          ag.kernels = launch_counter().load() - c0;
+          CK(cudaGraphInstantiate(&ag.exec, graph, 0));
+          CK(cudaGraphDestroy(graph));
+        } else {
+          launch_counter().fetch_add(ag.kernels, std::memory_order_relaxed);
+        }
+        CK(cudaGraphLaunch(ag.exec, s));
+        CK(cudaEventRecord(m->last, s));
+        return;
+      }
+    }
+    if (m->graphs.size() < 8) m->graphs.push_back(gdsw_precond::ApplyGraph{r, z, s, nullptr, 0});
+  }
   with_dtype(m->dtype, [&](auto tag) { apply_T<decltype(tag)>(m, r, z, s); });
   CK(cudaEventRecord(m->last, s));
 }
@@ -1193,6 +1242,7 @@ int gdsw_precond_create(gdsw_precond** out, gdsw_plan* plan, int dtype, int tris
     m->x3.alloc(nl);
     CK(cudaEventCreateWithFlags(&m->last, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&m->side, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&m->cap, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
     CK(cudaEventRecord(m->last, 0));
@@ -1217,6 +1267,7 @@ int gdsw_precond_set_coarse(gdsw_precond* m, const gdsw_coarse_desc* desc) {
     m->red64.alloc(2 * (size_t)std::max(cp->n_c, 1));
     CK(cudaDeviceSynchronize());
     m->cp = std::move(cp);
+    m->drop_graphs();
     m->has_phi = m->has_ainv = false;
   });
 }
@@ -1227,6 +1278,7 @@ int gdsw_precond_set_factors(gdsw_precond* m, const void* l_vals, const void* u_
     if (P->nnz_l) CK(cudaMemcpy(m->lval.p, l_vals, P->nnz_l * m->es, cudaMemcpyHostToDevice));
     if (P->nnz_u) CK(cudaMemcpy(m->uval.p, u_vals, P->nnz_u * m->es, cudaMemcpyHostToDevice));
     m->has_factors = true;
+    m->drop_graphs();
     m->jacobi_ready = false;
     m->sched_vals_ready = false;
     m->stream_vals_ready = false;
@@ -1292,6 +1344,7 @@ int gdsw_precond_lu_numeric(gdsw_precond* m, const gdsw_csr* a, double diag_shif
     std::vector<int64_t> f = fail.download();
     for (int32_t s = 0; s < P->n_sub; ++s) fail_rows[s] = f[s] == INT64_MAX ? 0 : f[s];
     m->has_factors = true;
+    m->drop_graphs();
     m->jacobi_ready = false;
     m->sched_vals_ready = false;
     m->stream_vals_ready = false;
@@ -1354,6 +1407,7 @@ int gdsw_precond_fastilu(gdsw_precond* m, const gdsw_csr* a, int sweeps, double*
                   "fixed-point factorization produced nonfinite entries; use a more conservative "
                   "initial guess (diagonal shift) or exact ILU");
     m->has_factors = true;
+    m->drop_graphs();
     m->jacobi_ready = false;
     m->sched_vals_ready = false;
     m->stream_vals_ready = false;
@@ -1463,6 +1517,7 @@ int gdsw_precond_extend(gdsw_precond* m, const gdsw_csr* a, double tol, int max_
     CK(cudaDeviceSynchronize());
     if (iters_out) *iters_out = it;
     m->has_phi = true;
+    m->drop_graphs();
   });
 }
 
@@ -1542,6 +1597,7 @@ int gdsw_precond_set_coarse_inverse(gdsw_precond* m, const double* a0inv) {
     std::vector<double> h(a0inv, a0inv + (size_t)P->n_c * P->n_c);
     with_dtype(m->dtype, [&](auto tag) { upload_cast<decltype(tag)>(m->ainv, h); });
     m->has_ainv = true;
+    m->drop_graphs();
   });
 }
 
