@@ -22,6 +22,7 @@
 #include "trisolve.cuh"
 #include "tristream.cuh"
 #include "jacobi_flow.cuh"
+#include "jacobi_tb.cuh"
 #include "lu_numeric.cuh"
 
 using namespace gdsw;
@@ -592,9 +593,19 @@ struct FlowPlan {
   DBuf<unsigned> done;      // [n_sweeps * n_chunks] epoch stamps
 };
 
+// tiles of the temporally blocked FastSpTRSV (jacobi_tb.cuh)
+struct TbPlan {
+  int iters = 0;
+  bool ok = false;
+  int32_t n_l = 0, n_u = 0;
+  size_t smem_l = 0, smem_u = 0;
+  DBuf<TbTile> lt, ut;
+};
+
 struct gdsw_precond {
   gdsw_plan* plan = nullptr;
   std::unique_ptr<FlowPlan> flow;
+  std::unique_ptr<TbPlan> tb;
   std::unique_ptr<CoarsePlan> cp;
   gdsw_dist* dist = nullptr;         // sharded layout (not owned)
   DBuf<double> part_ext, recv_ext;   // reverse-halo partial sums (ext-local)
@@ -794,6 +805,111 @@ FlowPlan* ensure_flow(gdsw_precond* m, int iters) {
   CK(cudaDeviceSynchronize());
   m->flow = std::move(F);
   return m->flow.get();
+}
+
+// Tiles for the temporally blocked sweeps: per block, the factor's reach K
+// (max |i - col| over its rows), tiles as large as two shared iterate
+// buffers over tile + s K halo rows allow. Not built (ok = false) when a
+// block's reach leaves tiles smaller than TB_MIN_ROWS -- the halo would
+// dominate -- or a factor is not a uniform narrow layout.
+constexpr int32_t TB_MIN_ROWS = 2048;
+constexpr size_t TB_SMEM = 227 * 1024;
+
+template <typename T>
+TbPlan* ensure_tb(gdsw_precond* m, int iters) {
+  if (m->tb && m->tb->iters == iters) return m->tb.get();
+  gdsw_plan* P = m->plan;
+  auto Tp = std::make_unique<TbPlan>();
+  Tp->iters = iters;
+  const int s = iters - 1;
+  const int64_t wmax = (int64_t)(TB_SMEM / (2 * sizeof(T)));
+  bool ok = s >= 1;
+  std::vector<TbTile> lt, ut;
+  int64_t wl = 0, wu = 0;
+  for (int32_t sd = 0; sd < P->n_sub && ok; ++sd) {
+    const int64_t r0 = P->h_sub_ptr[sd], r1 = P->h_sub_ptr[sd + 1], n = r1 - r0;
+    if (n == 0) continue;
+    int64_t kl = 0, ku = 0;
+    for (int64_t i = r0; i < r1; ++i) {
+      const int64_t li = i - r0;
+      for (int64_t q = P->h_l_ptr[i]; q < P->h_l_ptr[i + 1]; ++q) kl = std::max<int64_t>(kl, li - P->h_l_idx[q]);
+      for (int64_t q = P->h_u_ptr[i] + 1; q < P->h_u_ptr[i + 1]; ++q) ku = std::max<int64_t>(ku, P->h_u_idx[q] - li);
+    }
+    for (int f = 0; f < 2 && ok; ++f) {
+      const int64_t K = f == 0 ? kl : ku;
+      const int64_t rmax = wmax - (int64_t)s * K;
+      if (rmax < std::min<int64_t>(TB_MIN_ROWS, n)) {
+        ok = false;
+        break;
+      }
+      const int64_t nt = (n + rmax - 1) / rmax;
+      const int64_t R = (n + nt - 1) / nt;
+      for (int64_t a = r0; a < r1; a += R) {
+        const int64_t b = std::min(r1, a + R);
+        TbTile t{(int32_t)a, (int32_t)b, (int32_t)r0, (int32_t)r1, (int32_t)K, 0};
+        if (f == 0) {
+          lt.push_back(t);
+          wl = std::max<int64_t>(wl, b - std::max<int64_t>(r0, a - (int64_t)s * K));
+        } else {
+          ut.push_back(t);
+          wu = std::max<int64_t>(wu, std::min<int64_t>(r1, b + (int64_t)s * K) - a);
+        }
+      }
+    }
+  }
+  ok = ok && P->l_sell.uw >= 1 && P->l_sell.uw <= 4 && P->u_sell.uw >= 1 && P->u_sell.uw <= 4;
+  Tp->ok = ok && !lt.empty();
+  if (Tp->ok) {
+    Tp->n_l = (int32_t)lt.size();
+    Tp->n_u = (int32_t)ut.size();
+    Tp->smem_l = (size_t)wl * 2 * sizeof(T);
+    Tp->smem_u = (size_t)wu * 2 * sizeof(T);
+    Tp->lt.upload(lt);
+    Tp->ut.upload(ut);
+  }
+  m->tb = std::move(Tp);
+  return m->tb.get();
+}
+
+// GDSW_JACOBI_TB=1: temporally blocked sweeps (jacobi_tb.cuh). Measured on
+// B200 at C2: HBM traffic of the L sweeps 560 -> 144 MB, but 1 CTA of 1024
+// threads per SM (shared-memory bound) and a barrier per sweep leave it
+// latency-bound: L 108 us / U 115 us vs 115 / 111 us for the per-sweep
+// launches, so it is off by default.
+bool jacobi_tb_enabled() { return env_flag("GDSW_JACOBI_TB"); }
+
+// both factors' sweeps in two launches (temporal blocking); returns the
+// buffer holding the block solutions
+template <typename T, bool D16>
+T* jacobi_tb_solve(gdsw_precond* m, TbPlan* Tp, const double* r, int iters, cudaStream_t s) {
+  gdsw_plan* P = m->plan;
+  T* B = (T*)m->xb.p;
+  T* F = (T*)m->x1.p;
+  T* Y = (T*)m->x2.p;
+  static bool attr = [] {
+    CK(cudaFuncSetAttribute(k_jacobi_tb_lower<T, D16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
+    CK(cudaFuncSetAttribute(k_jacobi_tb_upper<T, D16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
+    return true;
+  }();
+  (void)attr;
+  const double n = (double)P->n_loc, cb = D16 ? 2.0 : 4.0;
+  {
+    // algorithmic bytes: L once (values + stored columns + row lengths), the
+    // gather (gmap + r), B and F written
+    ProfScope ps("jacobi_tb_lower", s, (double)P->nnz_l * (sizeof(T) + cb) + n * 2.0 + n * 12.0 + 2.0 * n * sizeof(T));
+    k_jacobi_tb_lower<T, D16><<<Tp->n_l, TB_THREADS, Tp->smem_l, s>>>(P->l_sell.view(), (const T*)m->lsell.p,
+                                                                      Tp->lt.p, iters - 1, P->gmap.p, r, B, F);
+    CK_LAUNCH();
+  }
+  {
+    ProfScope ps("jacobi_tb_upper", s, (double)(P->nnz_u - P->n_loc) * (sizeof(T) + cb) + n * 2.0 +
+                                           3.0 * n * sizeof(T));
+    k_jacobi_tb_upper<T, D16><<<Tp->n_u, TB_THREADS, Tp->smem_u, s>>>(P->u_sell.view(), (const T*)m->usell.p,
+                                                                      Tp->ut.p, iters - 1, (const T*)m->udiag.p,
+                                                                      F, Y);
+    CK_LAUNCH();
+  }
+  return Y;
 }
 
 // all sweeps in one launch; same buffer rotation as jacobi_solve
@@ -1042,6 +1158,10 @@ T* local_solve(gdsw_precond* m, const double* r, int jacobi_iters, cudaStream_t 
     m->ensure_jacobi();
     const int it = jacobi_iters > 0 ? jacobi_iters : m->iters;
     const bool d16 = P->l_sell.has16 && P->u_sell.has16;
+    if (jacobi_tb_enabled() && it >= 2 && !jacobi_fused_enabled() && !jacobi_flow_enabled()) {
+      TbPlan* Tp = ensure_tb<T>(m, it);
+      if (Tp->ok) return d16 ? jacobi_tb_solve<T, true>(m, Tp, r, it, s) : jacobi_tb_solve<T, false>(m, Tp, r, it, s);
+    }
     if (jacobi_flow_enabled() && it >= 3 && !jacobi_fused_enabled()) {
       static const int rpt = [] {
         const char* e = std::getenv("GDSW_FLOW_RPT");
