@@ -246,6 +246,12 @@ int gdsw_gmres_dist(const gdsw_csr* a, gdsw_precond* m, const gdsw_csr* m_csr, c
  * out (host) receives 2(j+1) values: [V.v..., v.v, V.z..., v.z] */
 int gdsw_block_dot(const double* V, int64_t ldv, int32_t j, const double* v, const double* z,
                    int64_t n, double* out, void* stream);
+/* single-reduce update (krylov.py:346-351) with the pass-j scalars in device
+ * memory, coef = [a(0..j), p/delta(0..j), delta, corr]:
+ *   v[j] = (w - V a)/delta;  zm[j] = (mc - Zm a)/delta (skipped when Zm is
+ *   NULL);  w = zc/delta - V p/delta - corr v[j]    (rows of ld doubles) */
+int gdsw_sr_update(double* V, double* Zm, int64_t ld, int64_t n, int32_t j, const double* coef, double* w,
+                   const double* mc, const double* zc, void* stream);
 
 /* ------------------------------------------------------------------------
  * Instrumentation: per-phase device time (CUDA events on the launching

@@ -66,6 +66,8 @@ _SIGS = {
     "gdsw_plan_set_block_pattern": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "gdsw_precond_lu_numeric": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p]),
     "gdsw_precond_coarse_galerkin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gdsw_sr_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_void_p,
+                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "gdsw_precond_extend": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_void_p,
                                       C.c_void_p]),
     "gdsw_precond_panel_entries": (C.c_int64, [C.c_void_p]),
@@ -459,6 +461,12 @@ def gmres_dist(a_own: DeviceCsr, m_pre, b_own, x_own, x0_nonzero: bool, cfg,
                 residual_reductions=rep.residual_reductions, restarts=rep.restarts,
                 history=hist[:rep.n_history].copy(),
                 true_residuals=[(int(tit[k]), float(tres[k])) for k in range(rep.n_true)])
+
+
+def sr_update(V, Zm, j: int, coef, w, mc, zc, n: int):
+    """In-place single-reduce update of device tensors (gdsw_sr_update)."""
+    _ck(_lib.gdsw_sr_update(_ptr(V), _ptr(Zm), int(n), int(n), int(j), _ptr(coef), _ptr(w), _ptr(mc),
+                            _ptr(zc), stream_handle()))
 
 
 def block_dot(V, j: int, v, z, n: int) -> np.ndarray:

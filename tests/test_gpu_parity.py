@@ -375,3 +375,32 @@ def test_block_dot_matches_numpy():
                     torch.from_numpy(z).cuda(), n)
     want = np.concatenate([V @ v, [v @ v], V @ z, [v @ z]])
     assert np.allclose(out, want, rtol=1e-12, atol=1e-9)
+
+
+def test_sr_update_matches_reference_algebra():
+    """gdsw_sr_update against krylov.py:346-351 in numpy, with and without
+    the preconditioned basis."""
+    torch = _torch()
+    from paper_2304_04876_b200.device import sr_update
+    rng = np.random.default_rng(2)
+    n, j = 50_001, 7
+    V = rng.standard_normal((j + 1, n))
+    Zm = rng.standard_normal((j + 1, n))
+    w, mc, zc = (rng.standard_normal(n) for _ in range(3))
+    a, p = rng.standard_normal(j), rng.standard_normal(j)
+    delta, corr = 1.7, 0.3
+    coef = np.concatenate([a, p / delta, [delta, corr]])
+    vj = (w - a @ V[:j]) / delta
+    zj = (mc - a @ Zm[:j]) / delta
+    wn = zc / delta - (p / delta) @ V[:j] - corr * vj
+    for keep in (True, False):
+        Vd, Zd = torch.from_numpy(V.copy()).cuda(), torch.from_numpy(Zm.copy()).cuda()
+        wd = torch.from_numpy(w.copy()).cuda()
+        sr_update(Vd, Zd if keep else None, j, torch.from_numpy(coef).cuda(), wd,
+                  torch.from_numpy(mc).cuda(), torch.from_numpy(zc).cuda(), n)
+        assert np.allclose(Vd[j].cpu().numpy(), vj, rtol=1e-12, atol=1e-12)
+        assert np.allclose(wd.cpu().numpy(), wn, rtol=1e-12, atol=1e-12)
+        if keep:
+            assert np.allclose(Zd[j].cpu().numpy(), zj, rtol=1e-12, atol=1e-12)
+        else:
+            assert np.array_equal(Zd[j].cpu().numpy(), Zm[j])   # untouched
