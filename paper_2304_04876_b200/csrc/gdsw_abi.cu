@@ -19,7 +19,6 @@
 #include "krylov.cuh"
 #include "prof.cuh"
 #include "sparse.cuh"
-#include "trisolve.cuh"
 #include "tristream.cuh"
 #include "jacobi_flow.cuh"
 #include "jacobi_tb.cuh"
@@ -191,10 +190,8 @@ struct gdsw_plan {
   DBuf<int32_t> sub_ptr, gmap;
   DBuf<int64_t> l_ptr, u_ptr;
   DBuf<int32_t> l_col, u_col;
-  // host level schedules (block-local rows), for the scheduled SpTRSV
+  // host level schedules (block-local rows): streamed SpTRSV and numeric LU
   std::vector<int64_t> h_llev_sub, h_llev_ptr, h_llev_rows, h_ulev_sub, h_ulev_ptr, h_ulev_rows;
-  TriSched l_sched, u_sched;     // exact / ILU(k) level-set layouts
-  bool sched_ready = false;
   // numeric LU on the GPU: permuted block pattern of A + device schedules
   bool has_ab = false;
   int32_t n_max = 0;
@@ -225,12 +222,7 @@ struct gdsw_plan {
     sell_ready = true;
   }
 
-  void ensure_sched() {
-    if (sched_ready) return;
-    l_sched.build(n_sub, h_sub_ptr, h_l_ptr, h_l_idx, 0, h_llev_sub, h_llev_ptr, h_llev_rows);
-    u_sched.build(n_sub, h_sub_ptr, h_u_ptr, h_u_idx, 1, h_ulev_sub, h_ulev_ptr, h_ulev_rows);
-    sched_ready = true;
-  }
+
   FastIluDev fastilu_dev() const {
     return FastIluDev{nnz_l, nnz_u, a_of.p, fi_ptr.p, fi_pl.p, fi_pu.p, fi_ldiag.p};
   }
@@ -616,8 +608,6 @@ struct gdsw_precond {
   bool has_factors = false, jacobi_ready = false, has_phi = false, has_ainv = false;
   DBuf<char> lval, uval;           // CSR order
   DBuf<char> lsell, usell, udiag;  // Jacobi copies
-  DBuf<char> lsv, usv, sdiag;      // scheduled-SpTRSV copies (exact / ILU(k))
-  bool sched_vals_ready = false;
   TriStream tstream;               // streamed-SpTRSV layout (exact / ILU(k))
   bool stream_built = false, stream_vals_ready = false;
   DBuf<double> panel64;
@@ -654,35 +644,6 @@ struct gdsw_precond {
   }
   const void* panel() const { return dtype == GDSW_F32 ? (const void*)panel32.p : (const void*)panel64.p; }
 
-  void ensure_sched_vals() {
-    if (sched_vals_ready) return;
-    gdsw_plan* P = plan;
-    P->ensure_sched();
-    lsv.alloc(std::max<int64_t>(P->l_sched.entries, 1) * es);
-    usv.alloc(std::max<int64_t>(P->u_sched.entries, 1) * es);
-    sdiag.alloc(std::max<int64_t>(P->n_loc, 1) * es);
-    CK(cudaMemset(lsv.p, 0, lsv.n));
-    CK(cudaMemset(usv.p, 0, usv.n));
-    with_dtype(dtype, [&](auto tag) {
-      using T = decltype(tag);
-      const dim3 blk(32, 8);
-      for (auto* pr : {&P->l_sched, &P->u_sched}) {
-        if (pr->n_place == 0) continue;
-        const bool up = pr == &P->u_sched;
-        k_sched_place<T><<<grid_for(pr->n_place, 8), blk>>>(pr->n_place, pr->pl_src.p, pr->pl_dst.p, pr->pl_len.p,
-                                                            pr->pl_stride.p, (const T*)(up ? uval.p : lval.p),
-                                                            (T*)(up ? usv.p : lsv.p));
-        CK_LAUNCH();
-      }
-      if (P->n_loc) {
-        k_extract_diag<T><<<grid_for(P->n_loc, TB), TB>>>((int32_t)P->n_loc, P->u_ptr.p, (const T*)uval.p,
-                                                          (T*)sdiag.p);
-        CK_LAUNCH();
-      }
-    });
-    CK(cudaDeviceSynchronize());
-    sched_vals_ready = true;
-  }
 
   void ensure_stream_vals() {
     if (stream_vals_ready) return;
@@ -1076,76 +1037,42 @@ void launch_stream(gdsw_precond* m, const double* r, T* y, int32_t ring, size_t 
 template <typename T>
 T* levelset_solve(gdsw_precond* m, const double* r, cudaStream_t s) {
   gdsw_plan* P = m->plan;
-  static const bool sched = env_flag("GDSW_TS_SCHED");
-  if (!sched) {
-    m->ensure_stream_vals();
-    const TriStream& ts = m->tstream;
-    // algorithmic bytes: L and U entries once (value + stored column
-    // width), U's diagonal, the gather (gmap + r) and the block solution
-    ProfScope ps("levelset", s, (double)(P->nnz_l + P->nnz_u - P->n_loc) * (sizeof(T) + ts.csize) +
-                                    P->n_loc * (12.0 + 2 * sizeof(T)));
-    T* y = (T*)m->x1.p;
-    // shared memory per CTA: the iterate goes to shared memory when it
-    // leaves a ring of at least 4 chunks
-    static const int64_t ring_env = [] {
-      const char* e = std::getenv("GDSW_TS_BUDGET_KB");
-      return e ? (int64_t)std::atoi(e) * 1024 : (int64_t)0;
-    }();
-    // measured on B200: the iterate in shared memory beats global/L1 as
-    // soon as it fits next to a ring of >= 4 chunks (C1 1.20 -> 0.87 ms,
-    // C3-sized blocks 2.11 -> 1.67 ms per solve); prefer a budget that keeps
-    // two CTAs per SM; an iterate in global memory wants a mid-size ring
-    // (L1 left for its gathers: C2 ILU(0) 0.71 -> 0.60 ms)
-    static const int64_t min_chunks = [] {
-      const char* e = std::getenv("GDSW_TS_MINCHUNKS");
-      return e ? (int64_t)std::atoi(e) : (int64_t)4;
-    }();
-    const int64_t xs = ts.max_rows * (int64_t)sizeof(T);
-    const int64_t need = xs + min_chunks * ts.chunk_max;
-    int64_t budget = need <= 110 * 1024 ? 110 * 1024 : (need <= 220 * 1024 ? 220 * 1024 : 160 * 1024);
-    if (ring_env) budget = ring_env;
-    const bool smx = budget - xs >= min_chunks * ts.chunk_max && !env_flag("GDSW_TS_XGLOBAL");
-    const int64_t ring = std::max<int64_t>(2LL * ts.chunk_max, ((smx ? budget - xs : budget) & ~int64_t(15)));
-    const size_t smem = (size_t)ring + (smx ? (size_t)xs : 0);
-    require(smem <= 220 * 1024, "streamed SpTRSV chunk too large");
-    if (ts.csize == 2) {
-      if (smx) launch_stream<T, uint16_t, true>(m, r, y, (int32_t)ring, smem, s);
-      else launch_stream<T, uint16_t, false>(m, r, y, (int32_t)ring, smem, s);
-    } else {
-      if (smx) launch_stream<T, int32_t, true>(m, r, y, (int32_t)ring, smem, s);
-      else launch_stream<T, int32_t, false>(m, r, y, (int32_t)ring, smem, s);
-    }
-    CK_LAUNCH();
-    return y;
-  }
-  m->ensure_sched_vals();
-  // algorithmic bytes: L and U entries once (value + 4 B column), U's
-  // diagonal, the gather (gmap + r) and the block solution
-  ProfScope ps("levelset", s, (double)(P->nnz_l + P->nnz_u - P->n_loc) * (sizeof(T) + 4) +
+  m->ensure_stream_vals();
+  const TriStream& ts = m->tstream;
+  // algorithmic bytes: L and U entries once (value + stored column
+  // width), U's diagonal, the gather (gmap + r) and the block solution
+  ProfScope ps("levelset", s, (double)(P->nnz_l + P->nnz_u - P->n_loc) * (sizeof(T) + ts.csize) +
                                   P->n_loc * (12.0 + 2 * sizeof(T)));
-  const size_t smem = (size_t)P->l_sched.max_rows * sizeof(T);
-  constexpr size_t SMEM_MAX = 200 * 1024;
   T* y = (T*)m->x1.p;
-  auto go = [&](auto kern, size_t sm) {
-    kern<<<P->n_sub, TS_THREADS, sm, s>>>(P->l_sched.view(), P->u_sched.view(), (const T*)m->lsv.p,
-                                          (const T*)m->usv.p, (const T*)m->sdiag.p, P->sub_ptr.p, P->gmap.p, r,
-                                          y);
-  };
-  static const bool simple = env_flag("GDSW_TS_SIMPLE");
-  if (smem <= SMEM_MAX) {
-    static bool attr_set = [] {
-      CK(cudaFuncSetAttribute(k_trisolve_sched<T, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)SMEM_MAX));
-      CK(cudaFuncSetAttribute(k_trisolve_sched<T, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)SMEM_MAX));
-      return true;
-    }();
-    (void)attr_set;
-    if (simple) go(k_trisolve_sched<T, true, false>, smem);
-    else go(k_trisolve_sched<T, true, true>, smem);
+  // shared memory per CTA: the iterate goes to shared memory when it
+  // leaves a ring of at least 4 chunks
+  static const int64_t ring_env = [] {
+    const char* e = std::getenv("GDSW_TS_BUDGET_KB");
+    return e ? (int64_t)std::atoi(e) * 1024 : (int64_t)0;
+  }();
+  // measured on B200: the iterate in shared memory beats global/L1 as
+  // soon as it fits next to a ring of >= 4 chunks (C1 1.20 -> 0.87 ms,
+  // C3-sized blocks 2.11 -> 1.67 ms per solve); prefer a budget that keeps
+  // two CTAs per SM; an iterate in global memory wants a mid-size ring
+  // (L1 left for its gathers: C2 ILU(0) 0.71 -> 0.60 ms)
+  static const int64_t min_chunks = [] {
+    const char* e = std::getenv("GDSW_TS_MINCHUNKS");
+    return e ? (int64_t)std::atoi(e) : (int64_t)4;
+  }();
+  const int64_t xs = ts.max_rows * (int64_t)sizeof(T);
+  const int64_t need = xs + min_chunks * ts.chunk_max;
+  int64_t budget = need <= 110 * 1024 ? 110 * 1024 : (need <= 220 * 1024 ? 220 * 1024 : 160 * 1024);
+  if (ring_env) budget = ring_env;
+  const bool smx = budget - xs >= min_chunks * ts.chunk_max && !env_flag("GDSW_TS_XGLOBAL");
+  const int64_t ring = std::max<int64_t>(2LL * ts.chunk_max, ((smx ? budget - xs : budget) & ~int64_t(15)));
+  const size_t smem = (size_t)ring + (smx ? (size_t)xs : 0);
+  require(smem <= 220 * 1024, "streamed SpTRSV chunk too large");
+  if (ts.csize == 2) {
+    if (smx) launch_stream<T, uint16_t, true>(m, r, y, (int32_t)ring, smem, s);
+    else launch_stream<T, uint16_t, false>(m, r, y, (int32_t)ring, smem, s);
   } else {
-    if (simple) go(k_trisolve_sched<T, false, false>, 0);
-    else go(k_trisolve_sched<T, false, true>, 0);
+    if (smx) launch_stream<T, int32_t, true>(m, r, y, (int32_t)ring, smem, s);
+    else launch_stream<T, int32_t, false>(m, r, y, (int32_t)ring, smem, s);
   }
   CK_LAUNCH();
   return y;
@@ -1400,10 +1327,8 @@ int gdsw_precond_set_factors(gdsw_precond* m, const void* l_vals, const void* u_
     m->has_factors = true;
     m->drop_graphs();
     m->jacobi_ready = false;
-    m->sched_vals_ready = false;
     m->stream_vals_ready = false;
     if (P->method == GDSW_FAST_ILU) m->ensure_jacobi();
-    else if (env_flag("GDSW_TS_SCHED")) m->ensure_sched_vals();
     else m->ensure_stream_vals();
   });
 }
@@ -1466,10 +1391,8 @@ int gdsw_precond_lu_numeric(gdsw_precond* m, const gdsw_csr* a, double diag_shif
     m->has_factors = true;
     m->drop_graphs();
     m->jacobi_ready = false;
-    m->sched_vals_ready = false;
     m->stream_vals_ready = false;
     if (P->method == GDSW_FAST_ILU) m->ensure_jacobi();
-    else if (env_flag("GDSW_TS_SCHED")) m->ensure_sched_vals();
     else m->ensure_stream_vals();
   });
 }
@@ -1529,7 +1452,6 @@ int gdsw_precond_fastilu(gdsw_precond* m, const gdsw_csr* a, int sweeps, double*
     m->has_factors = true;
     m->drop_graphs();
     m->jacobi_ready = false;
-    m->sched_vals_ready = false;
     m->stream_vals_ready = false;
     m->ensure_jacobi();
   });

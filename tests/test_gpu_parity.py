@@ -68,7 +68,7 @@ def test_spmv_bitwise_against_oracle():
         assert np.array_equal(yy.cpu().numpy(), want - want)
 
 
-TS_CHAIN = 128   # trisolve.cuh: rows up to this length keep the sequential order
+TS_CHAIN = 128   # tristream.cuh TR_SEG: rows up to this length keep the sequential order
 LONG_ROW_TOL = 1e-13
 
 

@@ -1,4 +1,4 @@
-"""Time the batched local solve (scheduled SpTRSV) alone on a config:
+"""Time the batched local solve (streamed SpTRSV) alone on a config:
     python tools/profile_ts.py C1 | C3s | C2ilu  [reps]
 C3s = elasticity 32^3 with 4x4x4 boxes (C3's block size, 64 blocks)."""
 import sys
