@@ -18,6 +18,26 @@ constexpr int KDOT_ROWS = 32;  // rows per block-dot launch (basis rows + self)
 constexpr int KDOT_THREADS = 256;
 constexpr int KDOT_W2 = 2 * KDOT_ROWS;
 
+// device-side single-reduce scalars from the fused block (krylov.py:305-306,
+// 346-350), same operation order as the host copy
+__device__ __forceinline__ void sr_coef_compute(int j, const double* blk, double* coef) {
+  double aa = 0.0, ap = 0.0;
+  for (int r = 0; r < j; ++r) {
+    const double a = blk[2 * r], p = blk[2 * r + 1];
+    aa = rn_add(aa, rn_mul(a, a));
+    ap = rn_add(ap, rn_mul(a, p));
+  }
+  const double d2 = rn_sub(blk[2 * j], aa);
+  const double delta = d2 > 0.0 ? sqrt(d2) : 0.0;
+  for (int r = 0; r < j; ++r) {
+    coef[r] = blk[2 * r];
+    coef[j + r] = rn_div(blk[2 * r + 1], delta);
+  }
+  coef[2 * j] = delta;
+  coef[2 * j + 1] = rn_div(rn_sub(blk[2 * j + 1], ap), rn_mul(delta, delta));
+}
+
+
 // rows of the combined list [V[0..nv), v] restricted to [r0, r0 + nrc),
 // nrc <= NR. out[2*rr + {0,1}] = row . v, row . z  (rr = local row index).
 // Each thread owns element pairs (grid-stride, 16-byte loads) and keeps
@@ -29,7 +49,7 @@ template <int NR>
 __global__ void __launch_bounds__(KDOT_THREADS, NR > 8 ? 1 : 2) k_block_dot(
     int64_t n, const double* __restrict__ V, int64_t ldv, int nv, int r0, int nrc,
     const double* __restrict__ v, const double* __restrict__ z, double* __restrict__ partial,
-    double* __restrict__ out, unsigned* __restrict__ counter) {
+    double* __restrict__ out, unsigned* __restrict__ counter, double* __restrict__ coef) {
   constexpr int NW = KDOT_THREADS / 32;
   __shared__ double red[NW][2 * NR];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -150,26 +170,31 @@ __global__ void __launch_bounds__(KDOT_THREADS, NR > 8 ? 1 : 2) k_block_dot(
     s = warp_sum(s);
     if (lane == 0) out[k] = s;
   }
+  if (coef) {
+    // the whole block is in: the next update's scalars (k_sr_coef) here
+    __syncthreads();
+    if (threadIdx.x == 0) sr_coef_compute(nv, out, coef);
+  }
   if (threadIdx.x == 0) *counter = 0u;
 }
 
 // host dispatch on the row-count bucket
 inline void launch_block_dot(unsigned grid, cudaStream_t s, int64_t n, const double* V, int64_t ldv,
                              int nv, int r0, int nrc, const double* v, const double* z,
-                             double* partial, double* out, unsigned* counter) {
+                             double* partial, double* out, unsigned* counter, double* coef = nullptr) {
   if (nrc <= 4)
-    k_block_dot<4><<<grid, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out, counter);
+    k_block_dot<4><<<grid, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out, counter, coef);
   else if (nrc <= 8)
-    k_block_dot<8><<<grid, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out, counter);
+    k_block_dot<8><<<grid, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out, counter, coef);
   else if (nrc <= 16)  // 32+ running sums: one CTA per SM (launch bound), half the grid
     k_block_dot<16><<<(grid + 1) / 2, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out,
-                                                          counter);
+                                                          counter, coef);
   else if (nrc <= 24)
     k_block_dot<24><<<(grid + 1) / 2, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out,
-                                                          counter);
+                                                          counter, coef);
   else
     k_block_dot<32><<<(grid + 1) / 2, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out,
-                                                          counter);
+                                                          counter, coef);
 }
 
 // single-reduce update (krylov.py:346-351). coef = [a(0..j), p/delta(0..j),
@@ -263,20 +288,7 @@ __global__ void k_add(int64_t n, const double* __restrict__ x, const double* __r
 // blk: [a(0..j), b2] .v column at even slots, [p, q] at odd slots
 __global__ void k_sr_coef(int j, const double* __restrict__ blk, double* __restrict__ coef) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double aa = 0.0, ap = 0.0;
-  for (int r = 0; r < j; ++r) {
-    const double a = blk[2 * r], p = blk[2 * r + 1];
-    aa = rn_add(aa, rn_mul(a, a));
-    ap = rn_add(ap, rn_mul(a, p));
-  }
-  const double d2 = rn_sub(blk[2 * j], aa);
-  const double delta = d2 > 0.0 ? sqrt(d2) : 0.0;
-  for (int r = 0; r < j; ++r) {
-    coef[r] = blk[2 * r];
-    coef[j + r] = rn_div(blk[2 * r + 1], delta);
-  }
-  coef[2 * j] = delta;
-  coef[2 * j + 1] = rn_div(rn_sub(blk[2 * j + 1], ap), rn_mul(delta, delta));
+  sr_coef_compute(j, blk, coef);
 }
 
 // x_out = x + sum_r y[r] Zm[r]   (krylov.py:340, 361)
