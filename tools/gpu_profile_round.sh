@@ -1,6 +1,6 @@
 # ncu evidence for profiles/: launch list of one C2 solve + full captures
 mkdir -p gpurun_out
-R=${R:-r1d}
+R=${R:-r1e}
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
   --log-file gpurun_out/${R}_launches.csv python tools/profile_c2.py --solves 1 > gpurun_out/${R}_launch.log 2>&1
 for k in k_jacobi_upper k_sr_update k_block_dot k_sell_spmv k_prolong k_restrict_chunks k_gather_jacobi_lower; do
