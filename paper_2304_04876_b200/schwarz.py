@@ -510,8 +510,10 @@ def _gpu_lu_pays(spec, symbolics) -> bool:
     the parallel host kernel. Measured on B200 + the box's host: ILU(k) and
     exact factors with rows up to ~800 entries are 2.5-5x faster on the GPU
     (C1 2.9 -> 0.5 s, C2 ILU(0) 2.8 -> 1.0 s); the dense separator rows of
-    C3-sized elasticity blocks (1,495 entries) serialise it (6 s host vs
-    10 s GPU), so those stay on the host. GDSW_HOST_LU=1 / =0 forces."""
+    C3-sized elasticity blocks (1,495 entries) serialise it, which only pays
+    once there are enough blocks to fill the GPU (64 blocks: 6 s host vs
+    10 s GPU; C3's 512 blocks: 55 s host vs 47 s GPU, whole numeric phase).
+    GDSW_HOST_LU=1 / =0 forces."""
     import os
     force = os.environ.get("GDSW_HOST_LU", "")
     if force in ("0", "1"):
@@ -519,7 +521,7 @@ def _gpu_lu_pays(spec, symbolics) -> bool:
     if spec.method != "exact_lu":
         return True
     longest = max((int(np.diff(s.l_ptr).max(initial=0)) for s in symbolics), default=0)
-    return longest <= 1024
+    return longest <= 1024 or len(symbolics) >= 256
 
 
 def apply(m: TwoLevelPreconditioner, r):
