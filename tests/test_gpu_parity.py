@@ -404,3 +404,35 @@ def test_sr_update_matches_reference_algebra():
             assert np.allclose(Zd[j].cpu().numpy(), zj, rtol=1e-12, atol=1e-12)
         else:
             assert np.array_equal(Zd[j].cpu().numpy(), Zm[j])   # untouched
+
+
+def test_supernodal_chunks_on_dense_and_arrow_blocks():
+    """Exact factors with strictly nested row patterns take the streamed
+    SpTRSV's supernodal chunks (GEMV over the shared external pattern,
+    32-row diagonal tiles, panel updates): a dense block (one supernode, no
+    external pattern) and an arrow block (a dense separator coupled to every
+    earlier row), against the oracle's sequential substitution and a dense
+    solve."""
+    rng = np.random.default_rng(4)
+    n, m1 = 150, 90
+    d = rng.standard_normal((n, n))
+    dense = d @ d.T + n * np.eye(n)
+    arrow = np.zeros((n, n))
+    for i in range(m1):
+        arrow[i, i] = 4.0
+        if i + 1 < m1:
+            arrow[i, i + 1] = arrow[i + 1, i] = -1.0
+    c = rng.standard_normal((n - m1, m1))
+    arrow[m1:, :m1] = c
+    arrow[:m1, m1:] = c.T
+    s = rng.standard_normal((n - m1, n - m1))
+    arrow[m1:, m1:] = s @ s.T + 4 * n * np.eye(n - m1)
+    for mat in (dense, arrow):
+        a = CsrMatrix.from_dense(mat)
+        sym = ls.symbolic_lu(a, ls.order_natural(n))
+        fac = ls.numeric_lu(a, sym)
+        b = rng.standard_normal(n)
+        x = fac.solve(b)
+        want = O.levelset_solve(sym, fac.l_values, fac.u_values, b)
+        assert np.abs(x - want).max() <= 1e-12 * np.abs(want).max()
+        assert np.abs(mat @ x - b).max() <= 1e-10 * np.abs(b).max()
