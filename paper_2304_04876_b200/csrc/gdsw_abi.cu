@@ -628,10 +628,12 @@ struct gdsw_precond {
     int64_t kernels;
   };
   std::vector<ApplyGraph> graphs;
+  uint64_t gen = 1;  // bumped whenever graphs holding this precond's buffers go stale
   void drop_graphs() {
     for (auto& ag : graphs)
       if (ag.exec) cudaGraphExecDestroy(ag.exec);
     graphs.clear();
+    ++gen;
   }
   ~gdsw_precond() {
     drop_graphs();
@@ -1223,6 +1225,14 @@ void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
 // (its collectives spin on peers) or with GDSW_NO_GRAPH=1.
 bool apply_graph_ok(const gdsw_precond* m) {
   return !m->dist && !prof().on && !env_flag("GDSW_NO_GRAPH") && !env_flag("GDSW_NO_OVERLAP");
+}
+
+// the apply's launches enqueued into a stream that is being captured into a
+// larger graph (the GMRES pass graph): no event handshake, no nested graph
+void precond_apply_captured(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
+  require(m->has_factors, "preconditioner has no numeric factors");
+  std::lock_guard<std::mutex> g(m->mu);
+  with_dtype(m->dtype, [&](auto tag) { apply_T<decltype(tag)>(m, r, z, s); });
 }
 
 void precond_apply(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
