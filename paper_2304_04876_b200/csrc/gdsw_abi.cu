@@ -60,6 +60,14 @@ std::vector<int64_t> vec(const int64_t* p, size_t n) {
 
 constexpr int TB = 256;
 
+// process-wide generations: a captured graph is tied to the (operator,
+// preconditioner) objects AND their generation, so an object freed and
+// reallocated at the same address never matches a stale graph
+uint64_t next_generation() {
+  static std::atomic<uint64_t> g{0};
+  return ++g;
+}
+
 // GDSW_JACOBI_FUSED=1 selects the cluster-fused FastSpTRSV (one launch,
 // factors L2-resident); default is one launch per sweep, measured faster
 // on B200 until the fused kernel's latency chain is shortened
@@ -92,6 +100,7 @@ bool jacobi_fused_enabled() {
 // ===========================================================================
 struct gdsw_csr {
   int64_t nrows = 0, ncols = 0, nnz = 0;
+  uint64_t gen = next_generation();
   int dtype = GDSW_F64;
   SellPattern pat;
   DBuf<char> csr_val;   // values in CSR order (A.values indexing for setup gathers)
@@ -628,12 +637,12 @@ struct gdsw_precond {
     int64_t kernels;
   };
   std::vector<ApplyGraph> graphs;
-  uint64_t gen = 1;  // bumped whenever graphs holding this precond's buffers go stale
+  uint64_t gen = next_generation();  // renewed whenever graphs holding its buffers go stale
   void drop_graphs() {
     for (auto& ag : graphs)
       if (ag.exec) cudaGraphExecDestroy(ag.exec);
     graphs.clear();
-    ++gen;
+    gen = next_generation();
   }
   ~gdsw_precond() {
     drop_graphs();
