@@ -78,21 +78,9 @@ bool env_flag(const char* name) {
   return e && e[0] == '1';
 }
 
-bool l2_hints_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("GDSW_L2HINT");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
+bool l2_hints_enabled() { return env_flag("GDSW_L2HINT"); }
 
-bool jacobi_fused_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("GDSW_JACOBI_FUSED");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
+bool jacobi_fused_enabled() { return env_flag("GDSW_JACOBI_FUSED"); }
 }  // namespace
 
 // ===========================================================================

@@ -146,10 +146,10 @@ def test_large_block_streamed_sptrsv_bitwise(method, fill):
 
 @pytest.mark.parametrize("name", [n for n in sorted(CASES) if CASES[n][4] == "fast_ilu"])
 def test_fastsptrsv_dataflow_and_apply_overlap_variants(name):
-    """The opt-in dataflow (one persistent launch) and temporally blocked
-    (one launch per factor) FastSpTRSV variants are bit-identical to the
-    per-sweep launches; the apply with and without the side-stream coarse
-    overlap is bit-identical too."""
+    """The opt-in FastSpTRSV variants -- dataflow (one persistent launch),
+    temporally blocked (one launch per factor), cluster-fused, L2-hinted --
+    are bit-identical to the per-sweep launches; the apply with and without
+    the side-stream coarse overlap is bit-identical too."""
     import os
     torch = _torch()
     prob, dec, cfg, skel, pre = setup_case(name)
@@ -158,7 +158,7 @@ def test_fastsptrsv_dataflow_and_apply_overlap_variants(name):
     n_loc = skel._local_plan["n_loc"]
     y0 = torch.empty(n_loc, dtype=dt, device="cuda")
     pre._dev.local_solve(r, y0)
-    for var in ("GDSW_JACOBI_FLOW", "GDSW_JACOBI_TB"):
+    for var in ("GDSW_JACOBI_FLOW", "GDSW_JACOBI_TB", "GDSW_JACOBI_FUSED", "GDSW_L2HINT"):
         try:
             os.environ[var] = "1"
             for _ in range(3):   # several launches: epochs and tickets carry over
