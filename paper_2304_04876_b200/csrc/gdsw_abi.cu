@@ -1054,10 +1054,13 @@ T* levelset_solve(gdsw_precond* m, const double* r, cudaStream_t s) {
   // C3-sized blocks 2.11 -> 1.67 ms per solve); prefer a budget that keeps
   // two CTAs per SM; an iterate in global memory wants a mid-size ring
   // (L1 left for its gathers: C2 ILU(0) 0.71 -> 0.60 ms)
-  static const int64_t min_chunks = [] {
+  static const int64_t min_chunks_env = [] {
     const char* e = std::getenv("GDSW_TS_MINCHUNKS");
-    return e ? (int64_t)std::atoi(e) : (int64_t)4;
+    return e ? (int64_t)std::atoi(e) : (int64_t)0;
   }();
+  // ring depth in chunks: 3 of the large chunks used with <= one block per
+  // SM, 4 of the 16 KB ones otherwise
+  const int64_t min_chunks = min_chunks_env ? min_chunks_env : (P->n_sub > num_sms() ? 4 : 3);
   const int64_t xs = ts.max_rows * (int64_t)sizeof(T);
   const int64_t need = xs + min_chunks * ts.chunk_max;
   int64_t budget = need <= 110 * 1024 ? 110 * 1024 : (need <= 220 * 1024 ? 220 * 1024 : 160 * 1024);

@@ -111,16 +111,16 @@ struct TriStream {
     require(nseg_max <= TR_MAXW, "factor row too long for the streamed SpTRSV");
     const int64_t need = ChunkLayout((int)nseg_max, 0, true, vsize).data +
                          nseg_max * (ts_al16(TR_SEG * (int64_t)vsize) + ts_al16(TR_SEG * (int64_t)csize));
-    // measured on B200: with at most one block per SM, 32 KB chunks (and the
-    // larger ring they imply) are faster (C2 ILU(0) 0.46 -> 0.41 ms, C1
-    // 0.91 -> 0.86 ms, 64 C3-sized blocks 1.71 -> 1.54 ms per solve); with
+    // measured on B200: with at most one block per SM, 48 KB chunks (and the
+    // larger ring they imply) are faster (C2 ILU(0) 0.46 -> 0.39 ms, C1
+    // 0.91 -> 0.86 ms, 64 C3-sized blocks 1.71 -> 1.51 ms per solve); with
     // more blocks than SMs, 16 KB keeps two CTAs per SM (512 C3 blocks:
-    // 3.4 ms vs 5.6 ms)
+    // 3.4 ms vs 5.6 ms with 32 KB)
     static const int64_t chunk_env = [] {
       const char* e = std::getenv("GDSW_TS_CHUNK_KB");
       return e ? (int64_t)std::atoi(e) * 1024 : (int64_t)0;
     }();
-    const int64_t chunk_min = chunk_env ? chunk_env : (n_sub > num_sms() ? TR_CHUNK_MIN : 2 * TR_CHUNK_MIN);
+    const int64_t chunk_min = chunk_env ? chunk_env : (n_sub > num_sms() ? TR_CHUNK_MIN : 3 * TR_CHUNK_MIN);
     chunk_max = (int32_t)ts_al16(std::max<int64_t>(chunk_min, need));
 
     std::vector<unsigned char> buf;
