@@ -1058,12 +1058,15 @@ T* levelset_solve(gdsw_precond* m, const double* r, cudaStream_t s) {
     const char* e = std::getenv("GDSW_TS_MINCHUNKS");
     return e ? (int64_t)std::atoi(e) : (int64_t)0;
   }();
-  // ring depth in chunks: 3 of the large chunks used with <= one block per
-  // SM, 4 of the 16 KB ones otherwise
-  const int64_t min_chunks = min_chunks_env ? min_chunks_env : (P->n_sub > num_sms() ? 4 : 3);
+  // ring depth: at least 3 chunks
+  const int64_t min_chunks = min_chunks_env ? min_chunks_env : 3;
   const int64_t xs = ts.max_rows * (int64_t)sizeof(T);
   const int64_t need = xs + min_chunks * ts.chunk_max;
-  int64_t budget = need <= 110 * 1024 ? 110 * 1024 : (need <= 220 * 1024 ? 220 * 1024 : 160 * 1024);
+  // more blocks than SMs: three CTAs per SM when the iterate and a 3-chunk
+  // ring fit in 72 KB (512 C3 blocks: 3.43 -> 3.26 ms per solve)
+  int64_t budget = need <= 72 * 1024 && P->n_sub > num_sms()
+                       ? 72 * 1024
+                       : (need <= 110 * 1024 ? 110 * 1024 : (need <= 220 * 1024 ? 220 * 1024 : 160 * 1024));
   if (ring_env) budget = ring_env;
   const bool smx = budget - xs >= min_chunks * ts.chunk_max && !env_flag("GDSW_TS_XGLOBAL");
   const int64_t ring = std::max<int64_t>(2LL * ts.chunk_max, ((smx ? budget - xs : budget) & ~int64_t(15)));
