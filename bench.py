@@ -49,7 +49,7 @@ METRIC = "GDSW-GMRES solve s & iters to 1e-7, 3D Laplace 2M dof/GPU; apply HBM G
 # iterations of the reference on C2 (measured by running it)
 REFERENCE_ITERATIONS = {(128, 4, "fast_ilu(0,3,5)", "natural", "double"): 82}
 APPLY_PHASES = ("restrict_panels", "restrict_columns", "coarse_solve", "gather",
-                "gather_jacobi_lower", "jacobi_lower", "diag_solve", "jacobi_upper", "jacobi_flow", "levelset",
+                "gather_jacobi_lower", "jacobi_lower", "jacobi_lower_diag", "diag_solve", "jacobi_upper", "jacobi_flow", "levelset",
                 "prolong", "scatter")
 
 

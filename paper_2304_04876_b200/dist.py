@@ -144,6 +144,7 @@ class DistPreconditioner:
         for d in sets:
             blk = extract_submatrix(loc_ext, d, d)
             syms.append(build_symbolic(blk, spec, make_ordering(blk, config.ordering)))
+        self.local_symbolics = syms
         from .schwarz import local_plan_arrays
         self.plan = device.Plan(local_plan_arrays(sh.n_ext, sets, syms, spec.method, a_ext))
         vdt = np.float32 if single else np.float64
