@@ -210,6 +210,19 @@ int gdsw_gmres(const gdsw_csr* a, gdsw_precond* m, const gdsw_csr* m_csr, const 
                gdsw_solve_report* rep, double* history, int32_t* true_it, double* true_res,
                int32_t cap, void* stream);
 
+/* Host operators: the reference's duck-typed gmres operands (callables and
+ * objects with .apply, krylov.py:88-100). y = op(x) on host arrays of n
+ * doubles; a nonzero return aborts the solve (GDSW_E_TYPE, the caller keeps
+ * its own exception). a_fn is used when a == NULL, m_fn when m == NULL and
+ * m_csr == NULL; the GMRES vectors stay on the device, each operator call
+ * stages its vector through pinned host buffers (no pass graphs). */
+typedef int (*gdsw_host_op)(void* ctx, const double* x, double* y, int64_t n);
+int gdsw_gmres_host_ops(const gdsw_csr* a, gdsw_host_op a_fn, void* a_ctx, gdsw_precond* m,
+                        const gdsw_csr* m_csr, gdsw_host_op m_fn, void* m_ctx, int64_t n,
+                        const double* b, double* x, int x0_nonzero, const gdsw_krylov_cfg* cfg,
+                        gdsw_workspace* ws, gdsw_solve_report* rep, double* history,
+                        int32_t* true_it, double* true_res, int32_t cap, void* stream);
+
 /* ------------------------------------------------------------------------
  * Sharded solve: one process per GPU, each rank owns a
  * contiguous row range [own_lo, own_hi) of its extended local layout of

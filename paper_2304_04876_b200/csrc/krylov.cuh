@@ -18,6 +18,12 @@ constexpr int KDOT_ROWS = 32;  // rows per block-dot launch (basis rows + self)
 constexpr int KDOT_THREADS = 256;
 constexpr int KDOT_W2 = 2 * KDOT_ROWS;
 
+// r = b - r (residual of a host operator's product, krylov.py:164-170)
+__global__ void k_b_minus(int64_t n, const double* __restrict__ b, double* __restrict__ r) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) r[i] = b[i] - r[i];
+}
+
 // device-side single-reduce scalars from the fused block (krylov.py:305-306,
 // 346-350), same operation order as the host copy
 __device__ __forceinline__ void sr_coef_compute(int j, const double* blk, double* coef) {

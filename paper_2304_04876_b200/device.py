@@ -82,6 +82,10 @@ _SIGS = {
     "gdsw_gmres": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                              C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                              C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
+    "gdsw_gmres_host_ops": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                      C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
     "gdsw_block_dot": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,
                                  C.c_int64, C.c_void_p, C.c_void_p]),
     "gdsw_dist_create": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64,
@@ -386,6 +390,63 @@ def gmres_device(a_dev: DeviceCsr, m_pre: Precond | None, m_csr: DeviceCsr | Non
                         m_csr.handle if m_csr else None, _ptr(b), _ptr(x),
                         1 if x0_nonzero else 0, C.byref(kc), ws.handle, C.byref(rep),
                         _ptr(hist), _ptr(tit), _ptr(tres), cap, stream_handle()))
+    return dict(iterations=rep.iterations, converged=bool(rep.converged),
+                reduction_count=rep.reduction_count,
+                iteration_reductions=rep.iteration_reductions,
+                residual_reductions=rep.residual_reductions, restarts=rep.restarts,
+                history=hist[:rep.n_history].copy(),
+                true_residuals=[(int(tit[k]), float(tres[k])) for k in range(rep.n_true)])
+
+
+HOST_OP = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int64)
+
+
+class _HostOp:
+    """A Python operator (callable) as a gdsw_host_op. The first exception
+    it raises is kept and re-raised after the native solve returns."""
+
+    def __init__(self, fn):
+        self.fn = fn
+        self.error = None
+        self.c = HOST_OP(self._call)
+
+    def _call(self, _ctx, xp, yp, n):
+        try:
+            x = np.ctypeslib.as_array(xp, shape=(n,))
+            y = np.asarray(self.fn(x.copy()), dtype=np.float64)
+            if y.shape != (n,):
+                raise ValueError("operator dimensions do not match the vector")
+            np.ctypeslib.as_array(yp, shape=(n,))[:] = y
+            return 0
+        except BaseException as err:  # noqa: BLE001 -- surfaced after the native call
+            if self.error is None:
+                self.error = err
+            return 1
+
+
+def gmres_host_ops(a_dev, a_fn, m_pre, m_csr, m_fn, n: int, b, x, x0_nonzero: bool, cfg) -> dict:
+    """The native GMRES loop with host-side A and/or M (the reference's
+    callables and .apply objects); vectors b, x on the device."""
+    ws = workspace(n, cfg.restart)
+    kc = _KrylovCfg(cfg.restart, cfg.rel_tol, cfg.max_iters,
+                    1 if cfg.variant == "single_reduce" else 0,
+                    1 if cfg.orthogonalization == "cgs2" else 0)
+    rep = _Report()
+    cap = 2 * cfg.max_iters + 8
+    hist = np.zeros(cap, dtype=np.float64)
+    tit = np.zeros(cap, dtype=np.int32)
+    tres = np.zeros(cap, dtype=np.float64)
+    ops = [_HostOp(f) if f is not None else None for f in (a_fn, m_fn)]
+    fn_ptr = [C.cast(o.c, C.c_void_p) if o else None for o in ops]
+    code = _lib.gdsw_gmres_host_ops(a_dev.handle if a_dev else None, fn_ptr[0], None,
+                                    m_pre.handle if m_pre else None, m_csr.handle if m_csr else None,
+                                    fn_ptr[1], None, int(n), _ptr(b), _ptr(x), 1 if x0_nonzero else 0,
+                                    C.byref(kc), ws.handle, C.byref(rep), _ptr(hist), _ptr(tit),
+                                    _ptr(tres), cap, stream_handle())
+    for o in ops:
+        if o is not None and o.error is not None:
+            raise o.error
+    _ck(code)
     return dict(iterations=rep.iterations, converged=bool(rep.converged),
                 reduction_count=rep.reduction_count,
                 iteration_reductions=rep.iteration_reductions,

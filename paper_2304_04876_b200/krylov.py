@@ -71,11 +71,24 @@ class SolveReport:
     true_residuals: list
 
 
+def _host_operator(obj):
+    """The reference's fallbacks (krylov.py:93-98): `.apply` objects, then
+    callables; they run on the host, called with float64 numpy vectors."""
+    if hasattr(obj, "apply") and callable(obj.apply):
+        return obj.apply
+    if callable(obj):
+        return obj
+    raise TypeError("operator must be a CsrMatrix, expose .apply, or be callable")
+
+
 def _device_operators(a, m, n: int):
-    """Resolve (A, M) to device objects; the reference's duck typing
-    (krylov.py:88-100) restricted to operators that live on the GPU."""
+    """Resolve (A, M) with the reference's duck typing (krylov.py:88-100):
+    CsrMatrix / DeviceCsr / TwoLevelPreconditioner run on the GPU; other
+    `.apply` objects and callables become host operators.
+    Returns (a_dev, a_fn, m_pre, m_csr, m_fn)."""
     from . import device
     from .schwarz import TwoLevelPreconditioner
+    a_fn = m_fn = a_dev = None
     if isinstance(a, CsrMatrix):
         if a.nrows != n or a.ncols != n:
             raise ValueError("operator dimensions do not match the vector")
@@ -87,8 +100,7 @@ def _device_operators(a, m, n: int):
             raise ValueError("operator dimensions do not match the vector")
         a_dev = a
     else:
-        raise TypeError("operator must be a CsrMatrix (the B200 GMRES runs the operator on "
-                        "the device; host callables are not supported)")
+        a_fn = _host_operator(a)
     m_pre = m_csr = None
     if m is None:
         pass
@@ -105,9 +117,8 @@ def _device_operators(a, m, n: int):
     elif isinstance(m, device.DeviceCsr):
         m_csr = m
     else:
-        raise TypeError("preconditioner must be a TwoLevelPreconditioner, a CsrMatrix or None "
-                        "(it runs on the device)")
-    return a_dev, m_pre, m_csr
+        m_fn = _host_operator(m)
+    return a_dev, a_fn, m_pre, m_csr, m_fn
 
 
 def _report(out: dict, solve_s: float) -> SolveReport:
@@ -141,7 +152,7 @@ def gmres(a, m, b, cfg: KrylovConfig = KrylovConfig(), x0=None):
     else:
         bh = np.ascontiguousarray(b, dtype=np.float64)
         n = bh.shape[0]
-    a_dev, m_pre, m_csr = _device_operators(a, m, n)
+    a_dev, a_fn, m_pre, m_csr, m_fn = _device_operators(a, m, n)
     if x0 is None:
         xd = t.zeros(n, dtype=t.float64, device="cuda")
         nonzero = False
@@ -158,7 +169,10 @@ def gmres(a, m, b, cfg: KrylovConfig = KrylovConfig(), x0=None):
         nonzero = bool((xd != 0).any().item())
     if not on_device:
         bd = t.from_numpy(bh).cuda()
-    out = device.gmres_device(a_dev, m_pre, m_csr, bd, xd, nonzero, cfg)
+    if a_fn is None and m_fn is None:
+        out = device.gmres_device(a_dev, m_pre, m_csr, bd, xd, nonzero, cfg)
+    else:
+        out = device.gmres_host_ops(a_dev, a_fn, m_pre, m_csr, m_fn, n, bd, xd, nonzero, cfg)
     if host_tensor:
         x = xd.cpu()
     else:
