@@ -210,6 +210,16 @@ class DeviceCsr:
             self.handle = None
 
 
+def to_host(xd):
+    """Device tensor -> host tensor through the caching pinned allocator
+    (a pageable .cpu() of a 16 MB vector costs ~5 ms, this ~0.3 ms)."""
+    t = torch()
+    out = t.empty(xd.shape, dtype=xd.dtype, pin_memory=True)
+    out.copy_(xd, non_blocking=True)
+    t.cuda.current_stream().synchronize()
+    return out
+
+
 def device_csr(a) -> DeviceCsr:
     """Cached device copy of a host CsrMatrix (re-uploaded when its values
     object changes)."""

@@ -174,7 +174,7 @@ def gmres(a, m, b, cfg: KrylovConfig = KrylovConfig(), x0=None):
     else:
         out = device.gmres_host_ops(a_dev, a_fn, m_pre, m_csr, m_fn, n, bd, xd, nonzero, cfg)
     if host_tensor:
-        x = xd.cpu()
+        x = device.to_host(xd)
     else:
-        x = xd if on_device else xd.cpu().numpy()
+        x = xd if on_device else device.to_host(xd).numpy()
     return x, _report(out, time.perf_counter() - t0)

@@ -537,4 +537,4 @@ def apply(m: TwoLevelPreconditioner, r):
         raise ValueError(f"residual has length {r.shape}, operator size {m.n}")
     rd = t.from_numpy(r).cuda()
     z = m.apply_device(rd)
-    return z.cpu().numpy()
+    return device.to_host(z).numpy()
