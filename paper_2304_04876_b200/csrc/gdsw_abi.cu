@@ -1021,15 +1021,15 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   return cur;
 }
 
-template <typename T, typename CT, bool SMEMX>
+template <typename T, typename CT, bool SMEMX, bool FWD = false>
 void launch_stream(gdsw_precond* m, const double* r, T* y, int32_t ring, size_t smem, cudaStream_t s) {
   static bool attr = [] {
-    CK(cudaFuncSetAttribute(k_trisolve_stream<T, CT, SMEMX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            220 * 1024));
+    CK(cudaFuncSetAttribute(k_trisolve_stream<T, CT, SMEMX, FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            FWD ? 200 * 1024 : 220 * 1024));
     return true;
   }();
   (void)attr;
-  k_trisolve_stream<T, CT, SMEMX><<<m->plan->n_sub, TR_THREADS_ALL, smem, s>>>(
+  k_trisolve_stream<T, CT, SMEMX, FWD><<<m->plan->n_sub, TR_THREADS_ALL, smem, s>>>(
       m->tstream.view(), ring, m->plan->sub_ptr.p, m->plan->gmap.p, r, y);
 }
 
@@ -1072,11 +1072,18 @@ T* levelset_solve(gdsw_precond* m, const double* r, cudaStream_t s) {
   const int64_t ring = std::max<int64_t>(2LL * ts.chunk_max, ((smx ? budget - xs : budget) & ~int64_t(15)));
   const size_t smem = (size_t)ring + (smx ? (size_t)xs : 0);
   require(smem <= 220 * 1024, "streamed SpTRSV chunk too large");
+  // forwarding slots: only with the iterate in global memory; the static
+  // forwarding buffers (2 x TR_FWD values) come out of the budget
+  const bool fwd = ts.fwd && !smx;
+  if (fwd) require(smem + 2 * TR_FWD * sizeof(T) <= 220 * 1024 && smem <= 200 * 1024,
+                   "streamed SpTRSV chunk too large");
   if (ts.csize == 2) {
     if (smx) launch_stream<T, uint16_t, true>(m, r, y, (int32_t)ring, smem, s);
+    else if (fwd) launch_stream<T, uint16_t, false, true>(m, r, y, (int32_t)ring, smem, s);
     else launch_stream<T, uint16_t, false>(m, r, y, (int32_t)ring, smem, s);
   } else {
     if (smx) launch_stream<T, int32_t, true>(m, r, y, (int32_t)ring, smem, s);
+    else if (fwd) launch_stream<T, int32_t, false, true>(m, r, y, (int32_t)ring, smem, s);
     else launch_stream<T, int32_t, false>(m, r, y, (int32_t)ring, smem, s);
   }
   CK_LAUNCH();

@@ -37,6 +37,12 @@ constexpr int TR_CWARPS = 8;                    // consumer warps
 constexpr int TR_CTHREADS = 32 * TR_CWARPS;
 constexpr int TR_THREADS_ALL = TR_CTHREADS + 32;  // + producer warp
 constexpr int TR_SHORT = 32;
+// previous-chunk forwarding: short-row results of a chunk are also kept in
+// shared memory (slot = position in the chunk), and the next chunk reads
+// them there instead of from the global iterate (freshly stored values miss
+// L1, so every level would pay an L2 round trip)
+constexpr int TR_FWD = 1024;
+constexpr uint16_t TR_NOFWD = 0xFFFFu;
 constexpr int TR_SEG = 128;
 constexpr int TR_MAXW = 64;                     // warp tasks per chunk
 constexpr int TR_CHUNK_MIN = 16 * 1024;
@@ -76,6 +82,7 @@ struct TriStream {
   int64_t total = 0, n_chunks = 0, max_rows = 0;
   int32_t chunk_max = 0;
   int vsize = 8, csize = 4;
+  bool fwd = false;  // slices carry forwarding slots (iterate too large for shared memory)
   DBuf<unsigned char> bytes;
   DBuf<int32_t> ch_sub, ch_len;
   DBuf<int64_t> ch_off;
@@ -122,6 +129,13 @@ struct TriStream {
     }();
     const int64_t chunk_min = chunk_env ? chunk_env : (n_sub > num_sms() ? TR_CHUNK_MIN : 3 * TR_CHUNK_MIN);
     chunk_max = (int32_t)ts_al16(std::max<int64_t>(chunk_min, need));
+    // the iterate cannot sit in shared memory next to a 3-chunk ring: the
+    // slices carry forwarding slots (GDSW_TS_NOFWD=1 disables)
+    {
+      const char* e = std::getenv("GDSW_TS_NOFWD");
+      fwd = max_rows * vsize + 3 * (int64_t)chunk_max > 220 * 1024 && !(e && std::atoi(e) != 0);
+    }
+    std::vector<int32_t> ch_of, slot_of;  // chunk / slot of each short row of the current pass
 
     std::vector<unsigned char> buf;
     std::vector<int32_t> h_ch_sub(n_sub + 1), h_ch_len;
@@ -201,6 +215,22 @@ struct TriStream {
         put32(cl.stab + 16 * q + 0, (int32_t)voff);
         put32(cl.stab + 16 * q + 4, (int32_t)coff);
         put32(cl.stab + 16 * q + 8, sl.width);
+        if (fwd) {
+          // slot of each entry's column in the previous chunk, or TR_NOFWD
+          const int64_t foff = dp;
+          dp += ts_al16((int64_t)32 * sl.width * 2);
+          put32(cl.stab + 16 * q + 12, (int32_t)foff);
+          const int32_t prev = (int32_t)h_ch_off.size() - 1;
+          for (int64_t k = 0; k < (int64_t)32 * sl.width; ++k) std::memcpy(c + foff + 2 * k, &TR_NOFWD, 2);
+          for (int l = 0; l < (int)sl.rows.size(); ++l)
+            for (int32_t k = 0; k < sl.lens[l]; ++k) {
+              const int64_t col = idx[sl.srcs[l] + k];
+              if (ch_of[col] == prev && slot_of[col] >= 0 && slot_of[col] < TR_FWD) {
+                const uint16_t f = (uint16_t)slot_of[col];
+                std::memcpy(c + foff + 2 * ((int64_t)32 * k + l), &f, 2);
+              }
+            }
+        }
         for (int l = 0; l < 32; ++l) {
           const bool ok = l < (int)sl.rows.size();
           put32(cl.srow + 4 * (32 * q + l), ok ? sl.rows[l] : 0);
@@ -222,6 +252,12 @@ struct TriStream {
         }
       }
       require(dp == len, "internal: chunk layout mismatch");
+      if (fwd)
+        for (int q = 0; q < nsl; ++q)
+          for (int l = 0; l < (int)sls[q].rows.size(); ++l) {
+            ch_of[sls[q].rows[l]] = (int32_t)h_ch_off.size();
+            slot_of[sls[q].rows[l]] = 32 * q + l;
+          }
       h_ch_off.push_back(off);
       h_ch_len.push_back((int32_t)len);
       wts.clear();
@@ -340,6 +376,10 @@ struct TriStream {
         const std::vector<int64_t>& ptr = *f->ptr;
         const int64_t n_s = sub_ptr[s + 1] - base;
         const std::vector<int64_t>& idx = *f->idx;
+        if (fwd) {
+          ch_of.assign(n_s, -1);
+          slot_of.assign(n_s, -1);
+        }
         auto rlen = [&](int64_t i) { return ptr[base + i + 1] - ptr[base + i] - f->skip; };
         auto rcol = [&](int64_t i, int64_t k) { return idx[ptr[base + i] + f->skip + k]; };
         // supernodes: runs of rows whose patterns nest by one (dense diagonal
@@ -447,7 +487,8 @@ struct TriStream {
               sl.dsrc.push_back(ptr[g]);
               sl.width = std::max(sl.width, len);
             }
-            const int64_t db = ts_al16((int64_t)32 * sl.width * vsize) + ts_al16((int64_t)32 * sl.width * csize);
+            const int64_t db = ts_al16((int64_t)32 * sl.width * vsize) + ts_al16((int64_t)32 * sl.width * csize) +
+                               (fwd ? ts_al16((int64_t)32 * sl.width * 2) : 0);
             if (cur_bytes(wts.size(), sls.size() + 1, data_bytes + db) > chunk_max) flush();
             sls.push_back(std::move(sl));
             data_bytes += db;
@@ -593,8 +634,9 @@ __device__ __forceinline__ void ts_sn_chunk(const unsigned char* __restrict__ c,
   }
 }
 
-template <typename T, typename CT>
-__device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T* x, T* part) {
+template <typename T, typename CT, bool FWD>
+__device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T* x, T* part, const T* fprev,
+                                         T* fcur) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int4 hdr = *reinterpret_cast<const int4*>(c);
   if (hdr.w != TR_ROWS) {
@@ -660,6 +702,7 @@ __device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T*
     const int4 st = *reinterpret_cast<const int4*>(c + cl.stab + 16 * (t >> 5));
     const T* v = reinterpret_cast<const T*>(c + st.x) + (t & 31);
     const CT* cc = reinterpret_cast<const CT*>(c + st.y) + (t & 31);
+    const uint16_t* fs = FWD ? reinterpret_cast<const uint16_t*>(c + st.w) + (t & 31) : nullptr;
     T acc = x[row];
     for (int k0 = 0; k0 < len; k0 += 4) {
       T pv[4], xv[4];
@@ -667,7 +710,12 @@ __device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T*
       for (int u = 0; u < 4; ++u) {
         if (k0 + u < len) {
           pv[u] = v[32 * (k0 + u)];
-          xv[u] = x[cc[32 * (k0 + u)]];
+          if (FWD) {
+            const uint16_t f = fs[32 * (k0 + u)];
+            xv[u] = f != TR_NOFWD ? fprev[f] : x[cc[32 * (k0 + u)]];
+          } else {
+            xv[u] = x[cc[32 * (k0 + u)]];
+          }
         }
       }
 #pragma unroll
@@ -676,6 +724,7 @@ __device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T*
     }
     if (up) acc = rn_div(acc, reinterpret_cast<const T*>(c + cl.sdiag)[t]);
     x[row] = acc;
+    if (FWD && t < TR_FWD) fcur[t] = acc;
   }
   if (hdr.z & 4) {
     // rows split in segments: partials summed in segment order by the
@@ -699,7 +748,7 @@ __device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T*
 // TR_NT in flight; a chunk never wraps), block solution written to y
 constexpr int TR_NT = 16;
 
-template <typename T, typename CT, bool SMEMX>
+template <typename T, typename CT, bool SMEMX, bool FWD>
 __global__ void __launch_bounds__(TR_THREADS_ALL) k_trisolve_stream(TriStreamDev S, int32_t ring_bytes,
                                                                     const int32_t* __restrict__ sub_ptr,
                                                                     const int32_t* __restrict__ gmap,
@@ -709,6 +758,7 @@ __global__ void __launch_bounds__(TR_THREADS_ALL) k_trisolve_stream(TriStreamDev
   __shared__ uint64_t full[TR_NT], empty[TR_NT];
   __shared__ int32_t pos[TR_NT], foot[TR_NT];
   __shared__ T part[TR_MAXW];
+  __shared__ T fwdbuf[FWD ? 2 * TR_FWD : 1];
   const int s = blockIdx.x;
   const int32_t base = sub_ptr[s], ns = sub_ptr[s + 1] - base;
   const int c0 = S.ch_sub[s], c1 = S.ch_sub[s + 1];
@@ -771,7 +821,8 @@ __global__ void __launch_bounds__(TR_THREADS_ALL) k_trisolve_stream(TriStreamDev
   for (int i = 0; i < nch; ++i) {
     const int t = i % TR_NT;
     mbar_wait(&full[t], (uint32_t)((i / TR_NT) & 1));
-    ts_chunk<T, CT>(ring + pos[t], x, part);
+    ts_chunk<T, CT, FWD>(ring + pos[t], x, part, fwdbuf + ((i & 1) ^ 1) * (FWD ? TR_FWD : 0),
+                         fwdbuf + (i & 1) * (FWD ? TR_FWD : 0));
     consumer_bar();
     if (threadIdx.x == 0) mbar_arrive(&empty[t]);
   }
