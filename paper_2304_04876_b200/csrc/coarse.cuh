@@ -148,22 +148,30 @@ constexpr int CH_THREADS = 256;
 constexpr int CH_MAXK = 128;
 
 // partial[chunk_poff + c] = sum over the chunk's rows of P[c][row] r[row]
-// (r is read once per row, each panel column streamed coalesced)
+// (r is read once per row, each panel column streamed coalesced). Each of
+// the RS_THREADS threads owns rows t and t + RS_THREADS of the chunk and
+// adds its two products before the column's warp tree: half the shuffles
+// per element (the kernel is shuffle-bound, most of all in fp32).
+constexpr int RS_THREADS = CH_THREADS / 2;
 template <typename T>
-__global__ void __launch_bounds__(CH_THREADS) k_restrict_chunks(ChunkDev D, const T* __restrict__ panel,
+__global__ void __launch_bounds__(RS_THREADS) k_restrict_chunks(ChunkDev D, const T* __restrict__ panel,
                                                                 const double* __restrict__ r,
                                                                 T* __restrict__ partial) {
-  __shared__ T red[CH_THREADS / 32][CH_MAXK];
+  __shared__ T red[RS_THREADS / 32][CH_MAXK];
   const int32_t ch = blockIdx.x;
   const int32_t s = D.chunk_sub[ch];
   const int32_t ni = D.n_int[s];
   const int k = D.col_ptr[s + 1] - D.col_ptr[s];
-  const bool on = threadIdx.x < D.chunk_nrow[ch];
-  const int32_t row = D.chunk_row0[ch] + threadIdx.x;
-  const T rv = on ? (T)r[D.ch_g[(size_t)ch * CH_THREADS + threadIdx.x]] : T(0);
-  const T* pc = panel + D.panel_off[s] + row;
+  const int32_t nrow = D.chunk_nrow[ch];
+  const int t0 = threadIdx.x, t1 = threadIdx.x + RS_THREADS;
+  const bool on0 = t0 < nrow, on1 = t1 < nrow;
+  const T rv0 = on0 ? (T)r[D.ch_g[(size_t)ch * CH_THREADS + t0]] : T(0);
+  const T rv1 = on1 ? (T)r[D.ch_g[(size_t)ch * CH_THREADS + t1]] : T(0);
+  const T* pc = panel + D.panel_off[s] + D.chunk_row0[ch] + t0;
   for (int c = 0; c < k; ++c) {
-    T v = on ? ldg_stream(pc + (int64_t)c * ni) * rv : T(0);
+    const T* q = pc + (int64_t)c * ni;
+    T v = on0 ? ldg_stream(q) * rv0 : T(0);
+    if (on1) v += ldg_stream(q + RS_THREADS) * rv1;
     v = warp_sum(v);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][c] = v;
   }
@@ -171,7 +179,7 @@ __global__ void __launch_bounds__(CH_THREADS) k_restrict_chunks(ChunkDev D, cons
   for (int c = threadIdx.x; c < k; c += blockDim.x) {
     T acc = T(0);
 #pragma unroll
-    for (int w = 0; w < CH_THREADS / 32; ++w) acc += red[w][c];
+    for (int w = 0; w < RS_THREADS / 32; ++w) acc += red[w][c];
     partial[D.chunk_poff[ch] + c] = acc;
   }
 }

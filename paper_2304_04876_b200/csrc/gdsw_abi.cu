@@ -1154,7 +1154,7 @@ void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
     if (Cp->n_chunks > 0) {
       // panels once + r at interior rows (4 B index + 8 B value)
       ProfScope ps("restrict_panels", cs, (double)Cp->panel_entries * sizeof(T) + Cp->n_int_total * 12.0);
-      k_restrict_chunks<T><<<Cp->n_chunks, CH_THREADS, 0, cs>>>(D, (const T*)m->panel(), r, (T*)m->pdot.p);
+      k_restrict_chunks<T><<<Cp->n_chunks, RS_THREADS, 0, cs>>>(D, (const T*)m->panel(), r, (T*)m->pdot.p);
       CK_LAUNCH();
     }
     {
@@ -1637,7 +1637,7 @@ int gdsw_precond_coarse_galerkin(gdsw_precond* m, const gdsw_csr* a, double* a0_
       }
       spmv_T<double>(a, z.p, nullptr, y.p, 0, 1.0, 0.0, 0);
       if (Cp->n_chunks > 0) {
-        k_restrict_chunks<double><<<Cp->n_chunks, CH_THREADS>>>(D, m->panel64.p, y.p, part.p);
+        k_restrict_chunks<double><<<Cp->n_chunks, RS_THREADS>>>(D, m->panel64.p, y.p, part.p);
         CK_LAUNCH();
       }
       k_restrict_columns<double><<<nc, 256>>>(nc, Cp->pgt_ptr.p, Cp->pgt_row.p, pgt.p, y.p, Cp->cpart_ptr.p,
