@@ -152,7 +152,8 @@ constexpr int CH_MAXK = 128;
 // the RS_THREADS threads owns rows t and t + RS_THREADS of the chunk and
 // adds its two products before the column's warp tree: half the shuffles
 // per element (the kernel is shuffle-bound, most of all in fp32).
-constexpr int RS_THREADS = CH_THREADS / 2;
+constexpr int RS_ROWS = 4;
+constexpr int RS_THREADS = CH_THREADS / RS_ROWS;
 template <typename T>
 __global__ void __launch_bounds__(RS_THREADS) k_restrict_chunks(ChunkDev D, const T* __restrict__ panel,
                                                                 const double* __restrict__ r,
@@ -163,15 +164,21 @@ __global__ void __launch_bounds__(RS_THREADS) k_restrict_chunks(ChunkDev D, cons
   const int32_t ni = D.n_int[s];
   const int k = D.col_ptr[s + 1] - D.col_ptr[s];
   const int32_t nrow = D.chunk_nrow[ch];
-  const int t0 = threadIdx.x, t1 = threadIdx.x + RS_THREADS;
-  const bool on0 = t0 < nrow, on1 = t1 < nrow;
-  const T rv0 = on0 ? (T)r[D.ch_g[(size_t)ch * CH_THREADS + t0]] : T(0);
-  const T rv1 = on1 ? (T)r[D.ch_g[(size_t)ch * CH_THREADS + t1]] : T(0);
-  const T* pc = panel + D.panel_off[s] + D.chunk_row0[ch] + t0;
+  T rv[RS_ROWS];
+  bool on[RS_ROWS];
+#pragma unroll
+  for (int q = 0; q < RS_ROWS; ++q) {
+    const int t = threadIdx.x + q * RS_THREADS;
+    on[q] = t < nrow;
+    rv[q] = on[q] ? (T)r[D.ch_g[(size_t)ch * CH_THREADS + t]] : T(0);
+  }
+  const T* pc = panel + D.panel_off[s] + D.chunk_row0[ch] + threadIdx.x;
   for (int c = 0; c < k; ++c) {
-    const T* q = pc + (int64_t)c * ni;
-    T v = on0 ? ldg_stream(q) * rv0 : T(0);
-    if (on1) v += ldg_stream(q + RS_THREADS) * rv1;
+    const T* p = pc + (int64_t)c * ni;
+    T v = T(0);
+#pragma unroll
+    for (int q = 0; q < RS_ROWS; ++q)
+      if (on[q]) v += ldg_stream(p + q * RS_THREADS) * rv[q];
     v = warp_sum(v);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][c] = v;
   }
