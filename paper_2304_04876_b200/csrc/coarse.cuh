@@ -235,8 +235,20 @@ __device__ __forceinline__ void prolong_interior_chunk(int32_t ch, const ChunkDe
   const int32_t y0 = D.ch_y0[ft], ny = D.ch_ny[ft];
   const T* pr = panel + D.panel_off[s] + row;
   T zc = T(0);
-  for (int32_t c = D.col_ptr[s]; c < D.col_ptr[s + 1]; ++c, pr += ni)
-    zc = rn_add(zc, rn_mul(ldg_stream(pr), v[D.col_ids[c]]));
+  // loads of 8 columns in flight (the additions stay in column order)
+  const int32_t c0 = D.col_ptr[s], c1 = D.col_ptr[s + 1];
+  int32_t c = c0;
+  for (; c + 8 <= c1; c += 8, pr += 8 * (int64_t)ni) {
+    T pv[8], vv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      pv[u] = ldg_stream(pr + u * (int64_t)ni);
+      vv[u] = v[D.col_ids[c + u]];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) zc = rn_add(zc, rn_mul(pv[u], vv[u]));
+  }
+  for (; c < c1; ++c, pr += ni) zc = rn_add(zc, rn_mul(ldg_stream(pr), v[D.col_ids[c]]));
   T acc = RA.start<T>(g);
   if (ny > 0) acc = rn_add(acc, y[y0]);
   if (ny > 1)
