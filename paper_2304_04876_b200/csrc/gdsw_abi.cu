@@ -20,8 +20,6 @@
 #include "prof.cuh"
 #include "sparse.cuh"
 #include "tristream.cuh"
-#include "jacobi_flow.cuh"
-#include "jacobi_tb.cuh"
 #include "lu_numeric.cuh"
 
 using namespace gdsw;
@@ -68,9 +66,6 @@ uint64_t next_generation() {
   return ++g;
 }
 
-// GDSW_JACOBI_FUSED=1 selects the cluster-fused FastSpTRSV (one launch,
-// factors L2-resident); default is one launch per sweep, measured faster
-// on B200 until the fused kernel's latency chain is shortened
 // GDSW_L2HINT=1 enables L2 evict_last hints on the Jacobi iterates
 // (measured slower on B200 at C2: off by default)
 bool env_flag(const char* name) {
@@ -80,7 +75,6 @@ bool env_flag(const char* name) {
 
 bool l2_hints_enabled() { return env_flag("GDSW_L2HINT"); }
 
-bool jacobi_fused_enabled() { return env_flag("GDSW_JACOBI_FUSED"); }
 }  // namespace
 
 // ===========================================================================
@@ -569,32 +563,8 @@ extern "C" int gdsw_plan_destroy(gdsw_plan* p) {
 // ===========================================================================
 // numeric preconditioner
 // ===========================================================================
-// work decomposition of the dataflow FastSpTRSV (jacobi_flow.cuh)
-struct FlowPlan {
-  int iters = 0, rpt = 0;
-  int32_t n_chunks = 0, n_groups = 0, n_sweeps = 0;
-  int64_t n_items = 0;
-  int grid = 0;
-  unsigned epoch = 0;
-  unsigned long long ticket_base = 0;
-  DBuf<int32_t> sub_chunk0, sub_row0, sub_reach, group_sub0;
-  DBuf<unsigned long long> ticket;
-  DBuf<unsigned> done;      // [n_sweeps * n_chunks] epoch stamps
-};
-
-// tiles of the temporally blocked FastSpTRSV (jacobi_tb.cuh)
-struct TbPlan {
-  int iters = 0;
-  bool ok = false;
-  int32_t n_l = 0, n_u = 0;
-  size_t smem_l = 0, smem_u = 0;
-  DBuf<TbTile> lt, ut;
-};
-
 struct gdsw_precond {
   gdsw_plan* plan = nullptr;
-  std::unique_ptr<FlowPlan> flow;
-  std::unique_ptr<TbPlan> tb;
   std::unique_ptr<CoarsePlan> cp;
   gdsw_dist* dist = nullptr;         // sharded layout (not owned)
   DBuf<double> part_ext, recv_ext;   // reverse-halo partial sums (ext-local)
@@ -611,7 +581,9 @@ struct gdsw_precond {
   DBuf<char> panel32;              // f32 copy when dtype == F32
   DBuf<char> pgr_val, pgt_val, ainv;
   DBuf<char> xb, x1, x2, x3, pdot, cu, cv;
-  std::mutex mu;
+  // recursive: a GMRES solve holds it for its whole duration and its
+  // eager passes re-enter precond_apply
+  std::recursive_mutex mu;
   cudaEvent_t last = nullptr;
   // side stream for the coarse restriction + solve, overlapped with the
   // local solves (fork/join by events; single-GPU path)
@@ -695,240 +667,6 @@ namespace {
 
 // FastSpTRSV: `iters` Jacobi iterates on L then U; returns the buffer
 // holding the block solutions
-// GDSW_JACOBI_FLOW=1: all sweeps in one persistent dataflow launch with
-// L2-resident subdomain groups (jacobi_flow.cuh). Measured on B200 at C2:
-// HBM traffic per apply drops from ~1.29 GB to ~0.33 GB, but the launch is
-// bound by the per-item dependent-load chain (309 us vs 270 us for the
-// per-sweep launches), so it is off by default.
-bool jacobi_flow_enabled() { return env_flag("GDSW_JACOBI_FLOW"); }
-
-// group subdomains so one group's factors + iterates fit the L2 budget
-template <typename T, bool D16, int RPT>
-FlowPlan* ensure_flow(gdsw_precond* m, int iters) {
-  constexpr int ROWS = JF_THREADS * RPT;
-  if (m->flow && m->flow->iters == iters && m->flow->rpt == RPT) return m->flow.get();
-  gdsw_plan* P = m->plan;
-  require(P->n_sub <= JF_MAXSUB, "too many subdomains for the dataflow FastSpTRSV");
-  auto F = std::make_unique<FlowPlan>();
-  F->iters = iters;
-  F->rpt = RPT;
-  F->n_sweeps = 2 * iters - 2;
-  require(F->n_sweeps <= JF_MAXSW, "too many Jacobi iterates for the dataflow kernel");
-  static const double budget = [] {
-    const char* e = std::getenv("GDSW_FLOW_MB");
-    return (e ? std::atof(e) : 80.0) * 1e6;
-  }();
-  const double cb = D16 ? 2.0 : 4.0;
-  std::vector<int32_t> sc0(P->n_sub + 1, 0), srow0(P->n_sub + 1, 0), reach(P->n_sub, 0), gsub0{0};
-  double ws = 0.0;
-  int32_t nch = 0;
-  for (int32_t sd = 0; sd < P->n_sub; ++sd) {
-    const int64_t r0 = P->h_sub_ptr[sd], r1 = P->h_sub_ptr[sd + 1];
-    const double nnz = (double)(P->h_l_ptr[r1] - P->h_l_ptr[r0]) + (double)(P->h_u_ptr[r1] - P->h_u_ptr[r0]);
-    const double b = nnz * (sizeof(T) + cb) + (double)(r1 - r0) * (4.0 + 5.0 * sizeof(T));
-    if (sd > gsub0.back() && ws + b > budget) {
-      gsub0.push_back(sd);
-      ws = 0.0;
-    }
-    ws += b;
-    sc0[sd] = nch;
-    srow0[sd] = (int32_t)r0;
-    nch += (int32_t)((r1 - r0 + ROWS - 1) / ROWS);
-    // reach: how many chunks away a row's columns can be (block-local)
-    int64_t K = 0;
-    for (int64_t i = r0; i < r1; ++i) {
-      const int64_t ci = (i - r0) / ROWS;
-      for (int64_t q = P->h_l_ptr[i]; q < P->h_l_ptr[i + 1]; ++q) K = std::max<int64_t>(K, ci - P->h_l_idx[q] / ROWS);
-      for (int64_t q = P->h_u_ptr[i]; q < P->h_u_ptr[i + 1]; ++q) K = std::max<int64_t>(K, P->h_u_idx[q] / ROWS - ci);
-    }
-    reach[sd] = (int32_t)K;
-    require(2 * K + 1 <= JF_THREADS, "factor reach too wide for the dataflow FastSpTRSV");
-  }
-  sc0[P->n_sub] = nch;
-  srow0[P->n_sub] = (int32_t)P->h_sub_ptr[P->n_sub];
-  gsub0.push_back(P->n_sub);
-  F->n_groups = (int32_t)gsub0.size() - 1;
-  require(F->n_groups <= JF_MAXGRP, "too many subdomain groups for the dataflow FastSpTRSV");
-  F->n_chunks = nch;
-  F->n_items = (int64_t)F->n_sweeps * nch;
-  F->sub_chunk0.upload(sc0);
-  F->sub_row0.upload(srow0);
-  F->sub_reach.upload(reach);
-  F->group_sub0.upload(gsub0);
-  F->ticket.alloc(1);
-  F->ticket.zero();
-  F->done.alloc(std::max<int64_t>((int64_t)F->n_sweeps * F->n_chunks, 1));
-  F->done.zero();
-  int nb = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_jacobi_flow<T, D16, RPT>, JF_THREADS, 0));
-  F->grid = std::max(1, nb) * num_sms();
-  CK(cudaDeviceSynchronize());
-  m->flow = std::move(F);
-  return m->flow.get();
-}
-
-// Tiles for the temporally blocked sweeps: per block, the factor's reach K
-// (max |i - col| over its rows), tiles as large as two shared iterate
-// buffers over tile + s K halo rows allow. Not built (ok = false) when a
-// block's reach leaves tiles smaller than TB_MIN_ROWS -- the halo would
-// dominate -- or a factor is not a uniform narrow layout.
-constexpr int32_t TB_MIN_ROWS = 2048;
-constexpr size_t TB_SMEM = 227 * 1024;
-
-template <typename T>
-TbPlan* ensure_tb(gdsw_precond* m, int iters) {
-  if (m->tb && m->tb->iters == iters) return m->tb.get();
-  gdsw_plan* P = m->plan;
-  auto Tp = std::make_unique<TbPlan>();
-  Tp->iters = iters;
-  const int s = iters - 1;
-  const int64_t wmax = (int64_t)(TB_SMEM / (2 * sizeof(T)));
-  bool ok = s >= 1;
-  std::vector<TbTile> lt, ut;
-  int64_t wl = 0, wu = 0;
-  for (int32_t sd = 0; sd < P->n_sub && ok; ++sd) {
-    const int64_t r0 = P->h_sub_ptr[sd], r1 = P->h_sub_ptr[sd + 1], n = r1 - r0;
-    if (n == 0) continue;
-    int64_t kl = 0, ku = 0;
-    for (int64_t i = r0; i < r1; ++i) {
-      const int64_t li = i - r0;
-      for (int64_t q = P->h_l_ptr[i]; q < P->h_l_ptr[i + 1]; ++q) kl = std::max<int64_t>(kl, li - P->h_l_idx[q]);
-      for (int64_t q = P->h_u_ptr[i] + 1; q < P->h_u_ptr[i + 1]; ++q) ku = std::max<int64_t>(ku, P->h_u_idx[q] - li);
-    }
-    for (int f = 0; f < 2 && ok; ++f) {
-      const int64_t K = f == 0 ? kl : ku;
-      const int64_t rmax = wmax - (int64_t)s * K;
-      if (rmax < std::min<int64_t>(TB_MIN_ROWS, n)) {
-        ok = false;
-        break;
-      }
-      const int64_t nt = (n + rmax - 1) / rmax;
-      const int64_t R = (n + nt - 1) / nt;
-      for (int64_t a = r0; a < r1; a += R) {
-        const int64_t b = std::min(r1, a + R);
-        TbTile t{(int32_t)a, (int32_t)b, (int32_t)r0, (int32_t)r1, (int32_t)K, 0};
-        if (f == 0) {
-          lt.push_back(t);
-          wl = std::max<int64_t>(wl, b - std::max<int64_t>(r0, a - (int64_t)s * K));
-        } else {
-          ut.push_back(t);
-          wu = std::max<int64_t>(wu, std::min<int64_t>(r1, b + (int64_t)s * K) - a);
-        }
-      }
-    }
-  }
-  ok = ok && P->l_sell.uw >= 1 && P->l_sell.uw <= 4 && P->u_sell.uw >= 1 && P->u_sell.uw <= 4;
-  Tp->ok = ok && !lt.empty();
-  if (Tp->ok) {
-    Tp->n_l = (int32_t)lt.size();
-    Tp->n_u = (int32_t)ut.size();
-    Tp->smem_l = (size_t)wl * 2 * sizeof(T);
-    Tp->smem_u = (size_t)wu * 2 * sizeof(T);
-    Tp->lt.upload(lt);
-    Tp->ut.upload(ut);
-  }
-  m->tb = std::move(Tp);
-  return m->tb.get();
-}
-
-// GDSW_JACOBI_TB=1: temporally blocked sweeps (jacobi_tb.cuh). Measured on
-// B200 at C2: HBM traffic of the L sweeps 560 -> 144 MB, but 1 CTA of 1024
-// threads per SM (shared-memory bound) and a barrier per sweep leave it
-// latency-bound: L 108 us / U 115 us vs 115 / 111 us for the per-sweep
-// launches, so it is off by default.
-bool jacobi_tb_enabled() { return env_flag("GDSW_JACOBI_TB"); }
-
-// both factors' sweeps in two launches (temporal blocking); returns the
-// buffer holding the block solutions
-template <typename T, bool D16>
-T* jacobi_tb_solve(gdsw_precond* m, TbPlan* Tp, const double* r, int iters, cudaStream_t s) {
-  gdsw_plan* P = m->plan;
-  T* B = (T*)m->xb.p;
-  T* F = (T*)m->x1.p;
-  T* Y = (T*)m->x2.p;
-  static bool attr = [] {
-    CK(cudaFuncSetAttribute(k_jacobi_tb_lower<T, D16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
-    CK(cudaFuncSetAttribute(k_jacobi_tb_upper<T, D16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TB_SMEM));
-    return true;
-  }();
-  (void)attr;
-  const double n = (double)P->n_loc, cb = D16 ? 2.0 : 4.0;
-  {
-    // algorithmic bytes: L once (values + stored columns + row lengths), the
-    // gather (gmap + r), B and F written
-    ProfScope ps("jacobi_tb_lower", s, (double)P->nnz_l * (sizeof(T) + cb) + n * 2.0 + n * 12.0 + 2.0 * n * sizeof(T));
-    k_jacobi_tb_lower<T, D16><<<Tp->n_l, TB_THREADS, Tp->smem_l, s>>>(P->l_sell.view(), (const T*)m->lsell.p,
-                                                                      Tp->lt.p, iters - 1, P->gmap.p, r, B, F);
-    CK_LAUNCH();
-  }
-  {
-    ProfScope ps("jacobi_tb_upper", s, (double)(P->nnz_u - P->n_loc) * (sizeof(T) + cb) + n * 2.0 +
-                                           3.0 * n * sizeof(T));
-    k_jacobi_tb_upper<T, D16><<<Tp->n_u, TB_THREADS, Tp->smem_u, s>>>(P->u_sell.view(), (const T*)m->usell.p,
-                                                                      Tp->ut.p, iters - 1, (const T*)m->udiag.p,
-                                                                      F, Y);
-    CK_LAUNCH();
-  }
-  return Y;
-}
-
-// all sweeps in one launch; same buffer rotation as jacobi_solve
-template <typename T, bool D16, int RPT>
-T* jacobi_flow_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
-  gdsw_plan* P = m->plan;
-  FlowPlan* F = ensure_flow<T, D16, RPT>(m, iters);
-  T* B = (T*)m->xb.p;
-  T* X1 = (T*)m->x1.p;
-  T* X2 = (T*)m->x2.p;
-  T* X3 = (T*)m->x3.p;
-  JfPlan J{};
-  J.L = P->l_sell.view();
-  J.U = P->u_sell.view();
-  J.sub_chunk0 = F->sub_chunk0.p;
-  J.sub_row0 = F->sub_row0.p;
-  J.sub_reach = F->sub_reach.p;
-  J.group_sub0 = F->group_sub0.p;
-  J.n_sub = P->n_sub;
-  J.rows_per_chunk = JF_THREADS * RPT;
-  J.gmap = P->gmap.p;
-  J.n_groups = F->n_groups;
-  J.n_chunks = F->n_chunks;
-  J.n_sweeps = F->n_sweeps;
-  J.n_items = F->n_items;
-  // every launch consumes exactly n_items + grid tickets; done stamps carry
-  // the launch epoch, so nothing is reset between launches
-  J.ticket = F->ticket.p;
-  J.ticket_base = F->ticket_base;
-  F->ticket_base += (unsigned long long)F->n_items + (unsigned long long)F->grid;
-  J.done = F->done.p;
-  J.epoch = ++F->epoch;
-  int t = 0;
-  J.sw[t++] = JfSweep{0, nullptr, X1, nullptr, B};
-  T* cur = X1;
-  T* oth = X2;
-  for (int k = 2; k < iters - 1; ++k) {
-    J.sw[t++] = JfSweep{1, cur, oth, B, nullptr};
-    std::swap(cur, oth);
-  }
-  J.sw[t++] = JfSweep{2, cur, oth, B, X3};
-  T* Fv = oth;
-  T* Gf = X3;
-  T* Hf = cur;
-  for (int k = 1; k < iters; ++k) {
-    J.sw[t++] = JfSweep{3, Gf, Hf, Fv, nullptr};
-    std::swap(Gf, Hf);
-  }
-  require(t == F->n_sweeps, "internal: dataflow sweep count");
-  const double n = (double)P->n_loc, cb = D16 ? 2.0 : 4.0;
-  // algorithmic bytes of the fused launch: both factors once (values +
-  // stored columns + row lengths), U's diagonal, the gather and the result
-  ProfScope ps("jacobi_flow", s, (double)P->nnz_l * (sizeof(T) + cb) + (double)(P->nnz_u - P->n_loc) * (sizeof(T) + cb) +
-                                     n * (4.0 + sizeof(T)) + n * 12.0 + n * sizeof(T));
-  k_jacobi_flow<T, D16, RPT><<<F->grid, JF_THREADS, 0, s>>>(J, (const T*)m->lsell.p, (const T*)m->usell.p,
-                                                      (const T*)m->udiag.p, r);
-  CK_LAUNCH();
-  return Gf;
-}
 
 template <typename T, bool HINT, bool D16, bool UNI>
 T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
@@ -942,20 +680,6 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   const double cb = D16 ? 2.0 : 4.0;  // stored column bytes per entry
   const double lbytes = (double)P->nnz_l * (sizeof(T) + cb) + n * (2.0 + 3 * sizeof(T));
   const double ubytes = (double)(P->nnz_u - n) * (sizeof(T) + cb) + n * (2.0 + 3 * sizeof(T));
-  if (jacobi_fused_enabled() && iters >= 1) {
-    // one cluster per subdomain, all iterates in one launch. Algorithmic
-    // bytes: both factors once (SELL values + columns + row lengths), U's
-    // diagonal, the gather (gmap + r) and the result; iterates stay in L2.
-    const double bytes = (double)P->nnz_l * (sizeof(T) + 4) + (double)(P->nnz_u - n) * (sizeof(T) + 4) +
-                         n * (2.0 * 2 + sizeof(T)) + n * 12.0 + n * (double)sizeof(T);
-    ProfScope ps("jacobi_fused", s, bytes);
-    JacobiClusterDev J{L, U, P->sub_ptr.p, P->gmap.p, iters};
-    k_jacobi_cluster<T><<<P->n_sub * JC_CLUSTER, JC_THREADS, 0, s>>>(
-        J, (const T*)m->lsell.p, (const T*)m->usell.p, (const T*)m->udiag.p, r, B, X1, X2);
-    CK_LAUNCH();
-    T* bufs[3] = {B, X1, X2};
-    return bufs[jc_result_buffer(iters)];
-  }
   // algorithmic bytes per launch: SELL values+columns once, row lengths,
   // b and x read once (gathers assumed cached), x_new written; the gather
   // variant reads r through gmap (4 + 8 per row, twice for the neighbours'
@@ -1097,21 +821,6 @@ T* local_solve(gdsw_precond* m, const double* r, int jacobi_iters, cudaStream_t 
     m->ensure_jacobi();
     const int it = jacobi_iters > 0 ? jacobi_iters : m->iters;
     const bool d16 = P->l_sell.has16 && P->u_sell.has16;
-    if (jacobi_tb_enabled() && it >= 2 && !jacobi_fused_enabled() && !jacobi_flow_enabled()) {
-      TbPlan* Tp = ensure_tb<T>(m, it);
-      if (Tp->ok) return d16 ? jacobi_tb_solve<T, true>(m, Tp, r, it, s) : jacobi_tb_solve<T, false>(m, Tp, r, it, s);
-    }
-    if (jacobi_flow_enabled() && it >= 3 && !jacobi_fused_enabled()) {
-      static const int rpt = [] {
-        const char* e = std::getenv("GDSW_FLOW_RPT");
-        return e ? std::atoi(e) : 2;
-      }();
-      if (rpt == 1)
-        return d16 ? jacobi_flow_solve<T, true, 1>(m, r, it, s) : jacobi_flow_solve<T, false, 1>(m, r, it, s);
-      if (rpt == 4)
-        return d16 ? jacobi_flow_solve<T, true, 4>(m, r, it, s) : jacobi_flow_solve<T, false, 4>(m, r, it, s);
-      return d16 ? jacobi_flow_solve<T, true, 2>(m, r, it, s) : jacobi_flow_solve<T, false, 2>(m, r, it, s);
-    }
     // uniform-width rows (all slots loaded at once): C2 sweeps 28.0/35.2/33.9
     // -> 25.9/30.2/27.8 us (GDSW_JACOBI_UNI=0 selects the plain loop)
     static const bool uni_off = [] {
@@ -1241,14 +950,14 @@ bool apply_graph_ok(const gdsw_precond* m) {
 // larger graph (the GMRES pass graph): no event handshake, no nested graph
 void precond_apply_captured(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
   require(m->has_factors, "preconditioner has no numeric factors");
-  std::lock_guard<std::mutex> g(m->mu);
+  std::lock_guard<std::recursive_mutex> g(m->mu);
   with_dtype(m->dtype, [&](auto tag) { apply_T<decltype(tag)>(m, r, z, s); });
 }
 
 void precond_apply(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
   require(m->has_factors, "preconditioner has no numeric factors");
   if (m->cp) require(m->has_phi && m->has_ainv, "coarse space is not set up");
-  std::lock_guard<std::mutex> g(m->mu);
+  std::lock_guard<std::recursive_mutex> g(m->mu);
   CK(cudaStreamWaitEvent(s, m->last, 0));
   if (apply_graph_ok(m)) {
     for (auto& ag : m->graphs) {
@@ -1670,7 +1379,7 @@ int gdsw_precond_apply(gdsw_precond* m, const double* r, double* z, void* stream
 int gdsw_precond_local_solve(gdsw_precond* m, const double* r, void* y, int jacobi_iters, void* stream) {
   return guarded([&] {
     require(m->has_factors, "preconditioner has no numeric factors");
-    std::lock_guard<std::mutex> g(m->mu);
+    std::lock_guard<std::recursive_mutex> g(m->mu);
     cudaStream_t s = S(stream);
     CK(cudaStreamWaitEvent(s, m->last, 0));
     with_dtype(m->dtype, [&](auto tag) {

@@ -381,130 +381,6 @@ __global__ void __launch_bounds__(256) k_gather_jacobi_lower(SellDev L,
 }
 
 // ---------------------------------------------------------------------------
-// Cluster-fused FastSpTRSV: one thread-block cluster per subdomain runs the
-// gather and ALL Jacobi iterates of L and U in one launch, with a cluster
-// barrier between iterates. While a cluster works on its subdomain, that
-// subdomain's factors (~3 MB) and iterates (~1 MB) stay in L2, so only the
-// first sweep of each factor streams from HBM (18 clusters of 8 CTAs are
-// resident at once: ~60 MB of L2). Per-row arithmetic is unchanged
-// (bit-identical to jacobi_trisolve_*); iterate reads go through L2
-// (ld.global.cg) because other CTAs of the cluster wrote them.
-// ---------------------------------------------------------------------------
-constexpr int JC_CLUSTER = 8;
-constexpr int JC_THREADS = 1024;
-
-struct JacobiClusterDev {
-  SellDev L, U;
-  const int32_t* sub_ptr;
-  const int32_t* gmap;
-  int iters;
-};
-
-__device__ __forceinline__ void cluster_barrier() {
-  __threadfence();
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
-                   : "memory");
-}
-
-// JC_ILP rows per thread per step, all their loads in flight together (the
-// per-row accumulation order is untouched)
-constexpr int JC_ILP = 4;
-
-template <typename T, bool UPPER>
-__device__ __forceinline__ void jc_rows(const SellDev& M, const T* __restrict__ val,
-                                        const T* __restrict__ diag, const T* b, const T* x, T* xn,
-                                        int32_t lo, int32_t a0, int32_t hi) {
-  for (int32_t i0 = a0 + threadIdx.x; i0 < hi; i0 += JC_ILP * blockDim.x) {
-    T acc[JC_ILP];
-#pragma unroll
-    for (int m = 0; m < JC_ILP; ++m) {
-      const int32_t i = i0 + m * blockDim.x;
-      const bool ok = i < hi && i >= lo;
-      const int32_t ic = ok ? i : lo;
-      const int64_t base = sell_base(M, ic);
-      const int len = ok ? M.row_len[ic] : 0;
-      acc[m] = sell_row<T, T, true, LdCg, false>(ok ? __ldcg(b + ic) : T(0), base, len, val, M, ic, x);
-    }
-#pragma unroll
-    for (int m = 0; m < JC_ILP; ++m) {
-      const int32_t i = i0 + m * blockDim.x;
-      if (i < hi && i >= lo) xn[i] = UPPER ? rn_div(acc[m], diag[i]) : acc[m];
-    }
-  }
-}
-
-template <typename T>
-__device__ __forceinline__ void jc_lower_rows(const SellDev& L, const T* __restrict__ lval,
-                                              const T* b, const T* x, T* xn, int32_t lo,
-                                              int32_t a0, int32_t hi) {
-  jc_rows<T, false>(L, lval, nullptr, b, x, xn, lo, a0, hi);
-}
-
-template <typename T>
-__device__ __forceinline__ void jc_upper_rows(const SellDev& U, const T* __restrict__ uval,
-                                              const T* __restrict__ diag, const T* b, const T* x,
-                                              T* xn, int32_t lo, int32_t a0, int32_t hi) {
-  jc_rows<T, true>(U, uval, diag, b, x, xn, lo, a0, hi);
-}
-
-// the buffer rotation (shared with the host, which needs the result buffer)
-__host__ __device__ inline int jc_result_buffer(int iters) {
-  // buffers: 0 = B, 1 = X1, 2 = X2 ; returns the buffer holding the U result
-  int F = 0;
-  if (iters >= 2) {
-    int cur = 1, oth = 2;
-    for (int t = 2; t < iters; ++t) { int tmp = cur; cur = oth; oth = tmp; }
-    F = cur;
-  }
-  int G = (F == 0) ? 1 : 0, H = (F == 2) ? 1 : 2;
-  if (F == 1) { G = 0; H = 2; }
-  int cur = G, oth = H;
-  for (int t = 1; t < iters; ++t) { int tmp = cur; cur = oth; oth = tmp; }
-  return cur;
-}
-
-template <typename T>
-__global__ void __cluster_dims__(JC_CLUSTER, 1, 1) __launch_bounds__(JC_THREADS, 1)
-    k_jacobi_cluster(JacobiClusterDev P, const T* __restrict__ lval, const T* __restrict__ uval,
-                     const T* __restrict__ diag, const double* __restrict__ r, T* B, T* X1, T* X2) {
-  const int s = blockIdx.x / JC_CLUSTER;
-  const int rank = blockIdx.x % JC_CLUSTER;
-  const int32_t lo = P.sub_ptr[s], hi = P.sub_ptr[s + 1];
-  // this CTA's slice-aligned share of the subdomain's rows
-  const int32_t alo = lo & ~31;
-  const int32_t piece = (((hi - alo + JC_CLUSTER - 1) / JC_CLUSTER) + 31) & ~31;
-  const int32_t a0 = alo + rank * piece;
-  const int32_t my_hi = min(hi, a0 + piece);
-  T* buf[3] = {B, X1, X2};
-  for (int32_t i = a0 + threadIdx.x; i < my_hi; i += blockDim.x)
-    if (i >= lo) B[i] = (T)r[P.gmap[i]];
-  cluster_barrier();
-  int F = 0;
-  if (P.iters >= 2) {
-    jc_lower_rows<T>(P.L, lval, B, B, X1, lo, a0, my_hi);
-    cluster_barrier();
-    int cur = 1, oth = 2;
-    for (int t = 2; t < P.iters; ++t) {
-      jc_lower_rows<T>(P.L, lval, B, buf[cur], buf[oth], lo, a0, my_hi);
-      cluster_barrier();
-      int tmp = cur; cur = oth; oth = tmp;
-    }
-    F = cur;
-  }
-  int G = (F == 0) ? 1 : 0, H = (F == 2) ? 1 : 2;
-  if (F == 1) { G = 0; H = 2; }
-  for (int32_t i = a0 + threadIdx.x; i < my_hi; i += blockDim.x)
-    if (i >= lo) buf[G][i] = rn_div(buf[F][i], diag[i]);
-  cluster_barrier();
-  int cur = G, oth = H;
-  for (int t = 1; t < P.iters; ++t) {
-    jc_upper_rows<T>(P.U, uval, diag, buf[F], buf[cur], buf[oth], lo, a0, my_hi);
-    cluster_barrier();
-    int tmp = cur; cur = oth; oth = tmp;
-  }
-}
-
-// ---------------------------------------------------------------------------
 // owner-computes scatter + coarse prolongation (schwarz.py:302-306, 322-327):
 //   z[g] = double( (Phi v)[g] + (((0 + y_a) + y_b) + ...) )
 // contributions y are summed in ascending subdomain order -- no atomics, the

@@ -10,6 +10,7 @@ library, or calling it without a CUDA device, raises.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 from pathlib import Path
 
 import numpy as np
@@ -221,13 +222,24 @@ def to_host(xd):
 
 
 def device_csr(a) -> DeviceCsr:
-    """Cached device copy of a host CsrMatrix (re-uploaded when its values
-    object changes)."""
+    """Cached float64 device copy of a host CsrMatrix (the GMRES operator is
+    float64: a float32 matrix is lifted once and the lifted copy cached).
+
+    The cache is keyed on the values array object, and that array is made
+    read-only while it backs a device copy: an in-place edit
+    (``a.values *= 2``) raises instead of silently solving with stale
+    values (the reference reads the current values on every spmv); assign a
+    new array, or build a new CsrMatrix, to change the operator."""
     cached = getattr(a, "_device_copy", None)
     if cached is not None and cached[0] is a.values:
         return cached[1]
-    d = DeviceCsr(a)
+    src = a
+    if a.values.dtype != np.float64:
+        from .sparse_core import CsrMatrix
+        src = CsrMatrix(a.nrows, a.ncols, a.row_ptr, a.col_idx, a.values.astype(np.float64))
+    d = DeviceCsr(src)
     try:
+        a.values.flags.writeable = False
         object.__setattr__(a, "_device_copy", (a.values, d))
     except Exception:
         pass
@@ -372,16 +384,20 @@ class Workspace:
             self.handle = None
 
 
-_WS: dict = {}
+_WS = threading.local()
 
 
 def workspace(n: int, restart: int) -> Workspace:
+    """The calling thread's Krylov workspace (V, Zm, the block slots and
+    pinned read-back buffers): per thread, so concurrent solves on different
+    threads never share it; at most one per thread (it holds 2*restart
+    vectors)."""
     key = (n, restart)
-    ws = _WS.get(key)
-    if ws is None:
-        _WS.clear()          # keep at most one (they hold 2*restart vectors)
-        ws = _WS[key] = Workspace(n, restart)
-    return ws
+    cur = getattr(_WS, "ws", None)
+    if cur is None or cur[0] != key:
+        _WS.ws = None
+        cur = _WS.ws = (key, Workspace(n, restart))
+    return cur[1]
 
 
 def gmres_device(a_dev: DeviceCsr, m_pre: Precond | None, m_csr: DeviceCsr | None, b, x,

@@ -81,6 +81,19 @@ def _host_operator(obj):
     raise TypeError("operator must be a CsrMatrix, expose .apply, or be callable")
 
 
+_IDENTITY: dict = {}
+
+
+def _identity(n: int) -> CsrMatrix:
+    eye = _IDENTITY.get(n)
+    if eye is None:
+        _IDENTITY.clear()
+        idx = np.arange(n, dtype=np.int64)
+        eye = _IDENTITY[n] = CsrMatrix(n, n, np.arange(n + 1, dtype=np.int64), idx,
+                                       np.ones(n, dtype=np.float64))
+    return eye
+
+
 def _device_operators(a, m, n: int):
     """Resolve (A, M) with the reference's duck typing (krylov.py:88-100):
     CsrMatrix / DeviceCsr / TwoLevelPreconditioner run on the GPU; other
@@ -89,12 +102,13 @@ def _device_operators(a, m, n: int):
     from . import device
     from .schwarz import TwoLevelPreconditioner
     a_fn = m_fn = a_dev = None
-    if isinstance(a, CsrMatrix):
+    if a is None:
+        # the reference's _operator(None) is the identity (krylov.py:89-90)
+        a_dev = device.device_csr(_identity(n))
+    elif isinstance(a, CsrMatrix):
         if a.nrows != n or a.ncols != n:
             raise ValueError("operator dimensions do not match the vector")
-        a_dev = device.device_csr(a if a.dtype == np.float64 else
-                                  CsrMatrix(a.nrows, a.ncols, a.row_ptr, a.col_idx,
-                                            a.values.astype(np.float64)))
+        a_dev = device.device_csr(a)
     elif isinstance(a, device.DeviceCsr):
         if a.nrows != n or a.ncols != n:
             raise ValueError("operator dimensions do not match the vector")
@@ -111,9 +125,7 @@ def _device_operators(a, m, n: int):
     elif isinstance(m, CsrMatrix):
         if m.nrows != n or m.ncols != n:
             raise ValueError("operator dimensions do not match the vector")
-        m_csr = device.device_csr(m if m.dtype == np.float64 else
-                                  CsrMatrix(m.nrows, m.ncols, m.row_ptr, m.col_idx,
-                                            m.values.astype(np.float64)))
+        m_csr = device.device_csr(m)
     elif isinstance(m, device.DeviceCsr):
         m_csr = m
     else:

@@ -49,6 +49,65 @@ BIG = {
 }
 
 
+# name: (kind, dims, parts, coarse, method, fill, sweeps, iters, precision, ordering, overlap)
+# BASELINE-scale configurations run by the reference (make_golden_configs.py)
+CONFIGS = {
+    # BASELINE configs[1] (C2) and its level-set companion
+    "C2_fast": ("laplace3d", (128, 128, 128), (4, 4, 4), "rgdsw", "fast_ilu", 0, 3, 5,
+                "double", "natural", 1),
+    "C2_ilu0": ("laplace3d", (128, 128, 128), (4, 4, 4), "rgdsw", "ilu_k", 0, 3, 5,
+                "double", "natural", 1),
+    # BASELINE configs[2] (C3): elasticity 64^3, exact LU + ND, P=8
+    "C3_ela64_exact_p8": ("elasticity3d", (64, 64, 64), (8, 8, 8), "rgdsw", "exact_lu", 0, 3,
+                          5, "double", "nested_dissection", 1),
+    # the subdomain sweep trend of configs[4] (C5) at 64^3
+    "lap64_fast_p2": ("laplace3d", (64, 64, 64), (2, 2, 2), "rgdsw", "fast_ilu", 0, 3, 5,
+                      "double", "natural", 1),
+    "lap64_fast_p4": ("laplace3d", (64, 64, 64), (4, 4, 4), "rgdsw", "fast_ilu", 0, 3, 5,
+                      "double", "natural", 1),
+    "lap64_fast_p8": ("laplace3d", (64, 64, 64), (8, 8, 8), "rgdsw", "fast_ilu", 0, 3, 5,
+                      "double", "natural", 1),
+    "lap64_ilu0_p2": ("laplace3d", (64, 64, 64), (2, 2, 2), "rgdsw", "ilu_k", 0, 3, 5,
+                      "double", "natural", 1),
+    "lap64_ilu0_p4": ("laplace3d", (64, 64, 64), (4, 4, 4), "rgdsw", "ilu_k", 0, 3, 5,
+                      "double", "natural", 1),
+    "lap64_ilu0_p8": ("laplace3d", (64, 64, 64), (8, 8, 8), "rgdsw", "ilu_k", 0, 3, 5,
+                      "double", "natural", 1),
+    "lap64_fast_p4_single": ("laplace3d", (64, 64, 64), (4, 4, 4), "rgdsw", "fast_ilu", 0, 3,
+                             5, "single", "natural", 1),
+    "lap64_ilu0_p8_single": ("laplace3d", (64, 64, 64), (8, 8, 8), "rgdsw", "ilu_k", 0, 3, 5,
+                             "single", "natural", 1),
+    # elasticity with the rigid-body coarse space
+    "ela24_exact_p4": ("elasticity3d", (24, 24, 24), (4, 4, 4), "rgdsw", "exact_lu", 0, 3, 5,
+                       "double", "nested_dissection", 1),
+    # BASELINE configs[3] (C4) shape at a size the reference's dense harmonic
+    # extension can finish: fp32 preconditioner, fast_ilu, P=5
+    "C4_lap100_single_p5": ("laplace3d", (100, 100, 100), (5, 5, 5), "rgdsw", "fast_ilu", 0, 3,
+                            5, "single", "natural", 1),
+}
+
+
+# configs whose full apply vector is stored (the rest keep a strided sample)
+FULL_APPLY = ("lap64_fast_p4", "lap64_fast_p4_single", "lap64_ilu0_p4", "ela24_exact_p4")
+
+# cases re-solved with a deliberately nonlinear operator (drift_operator):
+# the GMRES estimate passes rtol while the true residual does not
+DRIFT_CASES = ("lap10_fast_nat",)
+DRIFT_EPS = 0.02
+
+
+def drift_operator(a, eps: float):
+    """x -> A x + eps ||x|| u (u a fixed unit vector): not linear, so the
+    Givens estimate drifts from the true residual ||b - A x|| and the
+    true-residual confirmation fails (krylov.py:331-342)."""
+    u = np.random.default_rng(11).standard_normal(a.nrows)
+    u /= np.linalg.norm(u)
+
+    def op(x):
+        return a @ x + eps * np.linalg.norm(x) * u
+    return op
+
+
 def build(pkg, case, nullspace_needed=True):
     """Build (prob, dec, config) with module namespace `pkg` exposing
     model_problems, decomposition, schwarz, local_solvers."""

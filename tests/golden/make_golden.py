@@ -25,7 +25,7 @@ import schwarzdd.local_solvers as ls  # noqa: E402
 import schwarzdd.model_problems as mp  # noqa: E402
 import schwarzdd.schwarz as sw  # noqa: E402
 
-from cases import BIG, CASES, build, decomposition_hash, probes, rhs, sha  # noqa: E402
+from cases import BIG, CASES, DRIFT_CASES, build, decomposition_hash, probes, rhs, sha  # noqa: E402
 
 PKG = (mp, dd, sw, ls)
 
@@ -53,8 +53,10 @@ def one(name, case):
         arrays["a0_dense"] = pre.coarse.a0.to_dense()
         out["n_coarse"] = pre.coarse.a0.nrows
     x_star, b = rhs(prob)
-    for variant in ("single_reduce", "classic"):
-        x, rep = kr.gmres(prob.a, pre, b, kr.KrylovConfig(variant=variant))
+    for variant, orth in (("single_reduce", "mgs"), ("classic", "mgs"), ("classic_cgs2", "cgs2")):
+        kcfg = kr.KrylovConfig(variant=variant.split("_")[0] if variant.startswith("classic")
+                               else variant, orthogonalization=orth)
+        x, rep = kr.gmres(prob.a, pre, b, kcfg)
         arrays[f"hist_{variant}"] = rep.residual_history
         arrays[f"x_{variant}"] = x
         out[variant] = dict(iterations=rep.iterations, converged=rep.converged,
@@ -64,6 +66,25 @@ def one(name, case):
                             true_residuals=[(int(i), float(v)) for i, v in rep.true_residuals])
     np.savez_compressed(HERE / f"golden_{name}.npz", **arrays)
     return out
+
+
+def drift(name, case):
+    """A deliberately nonlinear host operator (tests/cases.py drift_operator):
+    the Givens estimate passes rel_tol while the true residual does not, so
+    the solve keeps iterating after failed confirmations and restarts
+    (krylov.py:331-342)."""
+    from cases import DRIFT_EPS, drift_operator
+    prob, dec, cfg = build(PKG, case)
+    skel = sw.setup_symbolic(prob.a, dec, cfg)
+    pre = sw.setup_numeric(skel, prob.a, prob.nullspace if cfg.use_coarse else None)
+    _, b = rhs(prob)
+    x, rep = kr.gmres(drift_operator(prob.a, DRIFT_EPS), pre, b,
+                      kr.KrylovConfig(variant="single_reduce", max_iters=60))
+    return dict(iterations=rep.iterations, converged=rep.converged, restarts=rep.restarts,
+                iteration_reductions=rep.iteration_reductions,
+                residual_reductions=rep.residual_reductions,
+                residual_history=[float(v) for v in rep.residual_history],
+                true_residuals=[(int(i), float(v)) for i, v in rep.true_residuals])
 
 
 def big(name, case):
@@ -91,6 +112,10 @@ def main():
     for name, case in CASES.items():
         print("case", name, flush=True)
         data["cases"][name] = one(name, case)
+    data.setdefault("drift", {})
+    for name in DRIFT_CASES:
+        print("drift", name, flush=True)
+        data["drift"][name] = drift(name, CASES[name])
     if "--big" in sys.argv:
         for name, case in BIG.items():
             print("big", name, flush=True)

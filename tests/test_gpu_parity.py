@@ -147,11 +147,10 @@ def test_large_block_streamed_sptrsv_bitwise(dims, method, fill):
 
 
 @pytest.mark.parametrize("name", [n for n in sorted(CASES) if CASES[n][4] == "fast_ilu"])
-def test_fastsptrsv_dataflow_and_apply_overlap_variants(name):
-    """The opt-in FastSpTRSV variants -- dataflow (one persistent launch),
-    temporally blocked (one launch per factor), cluster-fused, L2-hinted --
-    are bit-identical to the per-sweep launches; the apply with and without
-    the side-stream coarse overlap is bit-identical too."""
+def test_fastsptrsv_layout_and_apply_overlap_variants(name):
+    """The plain-loop FastSpTRSV rows (GDSW_JACOBI_UNI=0) and the L2-hinted
+    iterates are bit-identical to the default uniform-width sweeps; the apply
+    with and without the side-stream coarse overlap is bit-identical too."""
     import os
     torch = _torch()
     prob, dec, cfg, skel, pre = setup_case(name)
@@ -160,10 +159,10 @@ def test_fastsptrsv_dataflow_and_apply_overlap_variants(name):
     n_loc = skel._local_plan["n_loc"]
     y0 = torch.empty(n_loc, dtype=dt, device="cuda")
     pre._dev.local_solve(r, y0)
-    for var in ("GDSW_JACOBI_FLOW", "GDSW_JACOBI_TB", "GDSW_JACOBI_FUSED", "GDSW_L2HINT"):
+    for var, val in (("GDSW_L2HINT", "1"),):
         try:
-            os.environ[var] = "1"
-            for _ in range(3):   # several launches: epochs and tickets carry over
+            os.environ[var] = val
+            for _ in range(2):
                 y1 = torch.full((n_loc,), float("nan"), dtype=dt, device="cuda")
                 pre._dev.local_solve(r, y1)
                 assert torch.equal(y0, y1), var
@@ -233,20 +232,128 @@ def test_gmres_matches_reference(golden, golden_dir, name):
     prob, dec, cfg, skel, pre = setup_case(name)
     g = np.load(golden_dir / f"golden_{name}.npz")
     x_star, b = rhs(prob)
-    for variant in ("single_reduce", "classic"):
-        x, rep = gmres(prob.a, pre, b, KrylovConfig(variant=variant))
+    for variant, orth in (("single_reduce", "mgs"), ("classic", "mgs"), ("classic_cgs2", "cgs2")):
+        x, rep = gmres(prob.a, pre, b, KrylovConfig(variant=variant.split("_cgs2")[0],
+                                                    orthogonalization=orth))
         want = golden["cases"][name][variant]
         assert rep.converged
         assert abs(rep.iterations - want["iterations"]) <= 1
         assert rep.true_residuals[-1][1] <= 1e-7
         r = b - prob.a @ x
         assert np.linalg.norm(r) <= 1e-7 * np.linalg.norm(b) * 1.0001
+        if rep.iterations == want["iterations"]:
+            assert rep.residual_reductions == want["residual_reductions"]
+            assert rep.restarts == want["restarts"]
+            assert rep.iteration_reductions == want["iteration_reductions"]
+            assert [i for i, _ in rep.true_residuals] == [i for i, _ in want["true_residuals"]]
         if variant == "single_reduce" and rep.iterations == want["iterations"]:
             assert rep.iteration_reductions == rep.iterations
             # fp32 preconditioners round differently in the coarse sums
             rtol = 1e-4 if cfg.precision == "single" else 1e-6
             assert np.allclose(rep.residual_history, g[f"hist_{variant}"], rtol=rtol,
                                atol=1e-12)
+
+
+@pytest.mark.parametrize("graphs", [True, False])
+def test_gmres_drift_confirmation_failures(golden, graphs, monkeypatch):
+    """Failed true-residual confirmations (krylov.py:331-342): a nonlinear
+    host operator A makes the Givens estimate pass rtol while the true
+    residual does not, for ten iterations in a row, then the cycle restarts.
+    The pipelined single-reduce loop must keep the queued pass's scalars and
+    block intact across each failed check (candidate y and the true-residual
+    norm have their own buffers), so iterations, restarts and every true
+    residual follow the reference."""
+    from cases import DRIFT_EPS, drift_operator
+    if not graphs:
+        monkeypatch.setenv("GDSW_NO_GRAPH", "1")
+    prob, dec, cfg, skel, pre = setup_case("lap10_fast_nat")
+    _, b = rhs(prob)
+    want = golden["drift"]["lap10_fast_nat"]
+    x, rep = gmres(drift_operator(prob.a, DRIFT_EPS), pre, b,
+                   KrylovConfig(variant="single_reduce", max_iters=60))
+    assert rep.converged == want["converged"]
+    assert rep.iterations == want["iterations"]
+    assert rep.restarts == want["restarts"]
+    assert rep.residual_reductions == want["residual_reductions"]
+    assert [i for i, _ in rep.true_residuals] == [i for i, _ in want["true_residuals"]]
+    assert np.allclose([v for _, v in rep.true_residuals],
+                       [v for _, v in want["true_residuals"]], rtol=1e-5)
+    assert np.allclose(rep.residual_history, want["residual_history"], rtol=1e-5, atol=1e-14)
+
+
+def test_gmres_drift_with_device_operators_tight_tolerance():
+    """Device A and M (the graphed pass path): at rel_tol 1e-15 the estimate
+    falls below the attainable true residual, so every iteration after that
+    runs a failed confirmation with a pass already queued. The recurrence
+    must stay intact: the true residuals stay at the attainable floor (a
+    corrupted basis would blow them up) and match the eager path's."""
+    import os
+    prob, dec, cfg, skel, pre = setup_case("lap10_fast_nat")
+    _, b = rhs(prob)
+    kc = KrylovConfig(variant="single_reduce", rel_tol=1e-15, max_iters=50)
+    x, rep = gmres(prob.a, pre, b, kc)
+    assert len(rep.true_residuals) >= 5
+    res = np.array([v for _, v in rep.true_residuals])
+    assert np.all(np.isfinite(rep.residual_history))
+    assert res.max() <= 1e-12
+    assert np.linalg.norm(b - prob.a @ x) <= 1e-12 * np.linalg.norm(b)
+    os.environ["GDSW_NO_GRAPH"] = "1"
+    try:
+        x2, rep2 = gmres(prob.a, pre, b, kc)
+    finally:
+        del os.environ["GDSW_NO_GRAPH"]
+    assert rep2.iterations == rep.iterations
+    assert [i for i, _ in rep2.true_residuals] == [i for i, _ in rep.true_residuals]
+    assert np.array_equal(rep2.residual_history, rep.residual_history)
+
+
+def test_gmres_identity_operator_none():
+    """gmres(None, M, b): A is the identity (krylov.py:89-90)."""
+    prob, dec, cfg, skel, pre = setup_case("lap9_onelevel_ilu0")
+    b = probes(prob.a.nrows, ks=(4,))[0]
+    x, rep = gmres(None, None, b)
+    assert rep.converged and rep.iterations == 1
+    assert np.allclose(x, b, rtol=1e-12)
+
+
+def test_gmres_solve_and_apply_on_two_threads():
+    """A solve and standalone applies of the same preconditioner from two
+    threads: the solve holds the preconditioner for its duration, each
+    thread has its own Krylov workspace, results are bit-identical to the
+    sequential ones."""
+    from concurrent.futures import ThreadPoolExecutor
+    prob, dec, cfg, skel, pre = setup_case("lap10_fast_nat")
+    _, b = rhs(prob)
+    vecs = probes(prob.a.nrows, ks=range(20, 28))
+    want_z = [pre.apply(r) for r in vecs]
+    want_x, _ = gmres(prob.a, pre, b)
+
+    def solve(_):
+        return gmres(prob.a, pre, b)[0]
+    with ThreadPoolExecutor(max_workers=3) as ex:
+        fx = [ex.submit(solve, k) for k in range(3)]
+        fz = [ex.submit(pre.apply, r) for r in vecs]
+        got_x = [f.result() for f in fx]
+        got_z = [f.result() for f in fz]
+    for g in got_x:
+        assert np.array_equal(g, want_x)
+    for g, w in zip(got_z, want_z):
+        assert np.array_equal(g, w)
+
+
+def test_gmres_stale_operator_values_rejected():
+    """The device copy of A is keyed on its values array, which is made
+    read-only while cached: an in-place edit raises instead of silently
+    solving with stale values."""
+    a = mp.assemble_laplace3d(mp.Grid3D(6, 6, 6)).a
+    a = CsrMatrix(a.nrows, a.ncols, a.row_ptr, a.col_idx, a.values.copy())
+    b = probes(a.nrows, ks=(2,))[0]
+    x1, _ = gmres(a, None, b)
+    with pytest.raises(ValueError):
+        a.values *= 2.0
+    a2 = CsrMatrix(a.nrows, a.ncols, a.row_ptr, a.col_idx, a.values * 2.0)
+    x2, _ = gmres(a2, None, b)
+    assert np.allclose(x2, 0.5 * x1, rtol=1e-6)
 
 
 def test_gmres_against_oracle_identical_iterations():

@@ -61,8 +61,9 @@ def test_oracle_gmres_matches_reference(golden, golden_dir, name):
     prob, dec, cfg, ore = _oracle(name)
     g = np.load(golden_dir / f"golden_{name}.npz")
     _, b = rhs(prob)
-    for variant in ("single_reduce", "classic"):
-        x, rep = O.gmres(lambda v: O.csr_spmv(prob.a, v), ore.apply, b, variant=variant)
+    for variant, orth in (("single_reduce", "mgs"), ("classic", "mgs"), ("classic_cgs2", "cgs2")):
+        x, rep = O.gmres(lambda v: O.csr_spmv(prob.a, v), ore.apply, b,
+                         variant=variant.split("_cgs2")[0], orthogonalization=orth)
         want = golden["cases"][name][variant]
         assert rep["iterations"] == want["iterations"]
         assert rep["converged"] == want["converged"]
@@ -70,6 +71,23 @@ def test_oracle_gmres_matches_reference(golden, golden_dir, name):
         assert rep["residual_reductions"] == want["residual_reductions"]
         assert np.allclose(rep["history"], g[f"hist_{variant}"], rtol=1e-9, atol=1e-15)
         assert np.abs(x - g[f"x_{variant}"]).max() <= 1e-9 * np.abs(x).max()
+
+
+@pytest.mark.parametrize("name", ["lap10_fast_nat"])
+def test_oracle_gmres_drift_matches_reference(golden, name):
+    """Nonlinear operator: failed true-residual confirmations, then a restart
+    (krylov.py:331-342) -- the oracle follows the reference's path."""
+    from cases import DRIFT_EPS, drift_operator
+    prob, dec, cfg, ore = _oracle(name)
+    _, b = rhs(prob)
+    x, rep = O.gmres(drift_operator(prob.a, DRIFT_EPS), ore.apply, b, max_iters=60)
+    want = golden["drift"][name]
+    assert rep["iterations"] == want["iterations"]
+    assert rep["converged"] == want["converged"]
+    assert len(want["true_residuals"]) > 2
+    assert [i for i, _ in rep["true_residuals"]] == [i for i, _ in want["true_residuals"]]
+    assert np.allclose([v for _, v in rep["true_residuals"]],
+                       [v for _, v in want["true_residuals"]], rtol=1e-6)
 
 
 def test_oracle_coarse_basis_matches_reference(golden_dir):
