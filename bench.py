@@ -71,6 +71,8 @@ def parse():
     p.add_argument("--cpu-sample-iters", type=int, default=5)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--sharded", action="store_true",
+                   help="run the sharded (multi-GPU) code path even at one rank")
     p.add_argument("--profile-region", action="store_true",
                    help="cudaProfilerStart/Stop around the timed region (ncu --profile-from-start off)")
     return p.parse_args()
@@ -103,15 +105,17 @@ def build_problem(args):
     return prob, dec, build_problem_config(args)
 
 
-def workload(args, world: int = 1) -> dict:
+def workload(args, world: int = 1, sharded: bool = False) -> dict:
     n = args.n ** 3
-    if world > 1:
+    if world > 1 or sharded:
         par = (f"sharded x{world}: z-slabs of {args.parts ** 3} subdomains per GPU, global "
                f"{args.n}x{args.n}x{args.n * world} grid / {args.parts}x{args.parts}x"
                f"{args.parts * world} boxes; halos, coarse rhs and the GMRES block over "
                "libgdsw peer-memory collectives (CUDA IPC, NVLink)")
     else:
         par = "single GPU"
+    if os.environ.get("GDSW_SAME_DEVICE") == "1" and world > 1:
+        par += " -- every rank on cuda:0 (functional check; times are not a scaling measurement)"
     return {"workload": (f"C2: 3D Laplace 7-pt {args.n}^3 ({n:,} dof per GPU), "
                          f"{args.parts}x{args.parts}x{args.parts}={args.parts ** 3} subdomains "
                          f"per GPU, overlap 1, rGDSW, {args.solver} local solves, "
@@ -209,17 +213,23 @@ def native(args):
     if os.environ.get("GDSW_SAME_DEVICE") == "1":
         local = 0
     torch.cuda.set_device(local)
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if "MASTER_PORT" not in os.environ:
+            os.environ["MASTER_PORT"] = str(_free_port())
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         # bootstrap only (IPC handles, dense A0 partials, timing max); the data
         # path uses libgdsw's own peer-memory collectives
         tdist.init_process_group("gloo")
 
     def barrier():
-        if world > 1:
+        if sharded:
             tdist.barrier()
 
     def max_over_ranks(v: float) -> float:
-        if world == 1:
+        if not sharded:
             return v
         t = torch.tensor([v], dtype=torch.float64)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
@@ -227,7 +237,7 @@ def native(args):
 
     kcfg = KrylovConfig(variant="single_reduce")
     t0 = time.perf_counter()
-    if world == 1:
+    if not sharded:
         prob, dec, cfg = build_problem(args)
     else:
         from paper_2304_04876_b200.dist import build_sharded_problem
@@ -238,7 +248,7 @@ def native(args):
     x_star = np.random.default_rng(0).standard_normal(n)
     b = prob.a @ x_star
     t0 = time.perf_counter()
-    if world == 1:
+    if not sharded:
         skel = setup_symbolic(prob.a, dec, cfg)
         t_sym = time.perf_counter() - t0
         t0 = time.perf_counter()
@@ -306,7 +316,7 @@ def native(args):
     phases = device.prof_read()
     its = reps[-1].iterations
     xh = x.cpu().numpy()
-    if world > 1:
+    if sharded:
         pieces = [None] * world
         tdist.all_gather_object(pieces, xh)
         xh = np.concatenate(pieces)
@@ -332,7 +342,7 @@ def native(args):
     # one apply's wall time on the device (the coarse restriction overlaps
     # the local solves on a side stream, so the phase sum overstates it)
     apply_ms = app_ms / n_apply
-    if world == 1:
+    if not sharded:
         r_dev = torch.from_numpy(np.random.default_rng(1).standard_normal(n)).cuda()
         z_dev = torch.empty_like(r_dev)
         for _ in range(3):
@@ -356,7 +366,7 @@ def native(args):
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference generators (assemble_laplace3d), x*=default_rng(0)."
                 "standard_normal(n), b=A x*",
-        "config": workload(args, world),
+        "config": workload(args, world, sharded),
         "iterations": its, "converged": bool(reps[-1].converged),
         "ms_per_iteration": ms_step / max(its, 1),
         "true_rel_residual": true_res, "true_error": true_err,
@@ -379,7 +389,7 @@ def native(args):
     }
     if not args.no_e2e:
         bh = torch.from_numpy(b[g0:g1].copy()).pin_memory()
-        if world == 1:
+        if not sharded:
             def solve_host(bh):
                 return gmres(prob.a, pre, bh, kcfg)
         else:
@@ -404,12 +414,12 @@ def native(args):
         result["e2e"] = {"value": e2e_ms / 1e3, "unit": "s", "h2d_bytes_per_step": nb * world,
                          "d2h_bytes_per_step": (nb + 8 * 2 * 31 * repe.iterations) * world,
                          "api": ("paper_2304_04876_b200.krylov.gmres(A, M, pinned host b)"
-                                 if world == 1 else
+                                 if not sharded else
                                  "paper_2304_04876_b200.dist.DistPreconditioner.solve "
                                  "(pinned host b -> device, x -> host)")}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not sharded and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(args, prob, dec, cfg, skel, pre, b, its)
-    if world > 1:
+    if sharded:
         tdist.destroy_process_group()
     if rank == 0:
         print(json.dumps(result), flush=True)
@@ -494,8 +504,42 @@ def reference(args):
     }), flush=True)
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args) -> int | None:
+    """`bench.py --gpus N` (N > 1) outside torchrun: re-exec this script
+    under torch.distributed.run with N ranks, one per GPU (the driver's own
+    launch form), so the sharded solve runs instead of a silent 1-GPU one.
+    Returns the exit code, or None when no launch is needed."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    if args.impl == "reference":
+        return None      # rank 0's host work only: nothing to spread
+    if os.environ.get("GDSW_SAME_DEVICE") != "1":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"metric": METRIC, "n_gpus": args.gpus,
+                              "error": f"--gpus {args.gpus} but {have} CUDA device(s) visible "
+                                       "(GDSW_SAME_DEVICE=1 runs every rank on cuda:0 as a "
+                                       "functional check)"}), flush=True)
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    code = self_launch(args)
+    if code is not None:
+        sys.exit(code)
     if args.impl == "reference":
         reference(args)
     else:

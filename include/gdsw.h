@@ -161,8 +161,10 @@ int64_t gdsw_precond_panel_entries(const gdsw_precond* m);
 int gdsw_precond_get_panels(const gdsw_precond* m, double* panels);
 /* Galerkin product A0 = Phi^T A Phi on the GPU (coarse_matrix,
  * coarse_space.py:205-207) from the extension's float64 panels: column c =
- * restriction of A (Phi e_c); a0_dense gets n_c x n_c row-major float64 */
-int gdsw_precond_coarse_galerkin(gdsw_precond* m, const gdsw_csr* a, double* a0_dense);
+ * restriction of A (Phi e_c); a0_dense gets n_c x n_c row-major float64.
+ * pattern (optional, n_c x n_c bytes): 1 where the reference's SpGEMM creates
+ * an entry (structural product over |Phi| and |A|, computed zeros kept) */
+int gdsw_precond_coarse_galerkin(gdsw_precond* m, const gdsw_csr* a, double* a0_dense, uint8_t* pattern);
 /* dense A0^-1 (n_c x n_c, row-major, float64; cast to the precond dtype) */
 int gdsw_precond_set_coarse_inverse(gdsw_precond* m, const double* a0inv);
 /* z = Phi A0^-1 Phi^T r + sum_i R_i^T A_i^-1 R_i r  (apply, schwarz.py:290-327) */
@@ -249,6 +251,12 @@ int gdsw_dist_allreduce(gdsw_dist* d, const double* in, double* out, int64_t m, 
 int gdsw_dist_halo(gdsw_dist* d, double* x_ext, void* stream);
 int gdsw_dist_destroy(gdsw_dist* d);
 int gdsw_precond_set_dist(gdsw_precond* m, gdsw_dist* d);
+/* sharded Galerkin product A0 = Phi^T A Phi (coarse_space.py:205-207): a_own
+   is this rank's owned rows over its extended columns; the partial products
+   are summed over ranks in rank order on the device; a0_dense: n_c x n_c
+   row-major, identical on every rank */
+int gdsw_dist_coarse_galerkin(gdsw_precond* m, const gdsw_csr* a_own, gdsw_dist* d, double* a0_dense,
+                              uint8_t* pattern);
 /* b, x: owned rows only (n_own) */
 int gdsw_gmres_dist(const gdsw_csr* a, gdsw_precond* m, const gdsw_csr* m_csr, const double* b,
                     double* x, int x0_nonzero, const gdsw_krylov_cfg* cfg, gdsw_workspace* ws,

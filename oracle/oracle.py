@@ -417,13 +417,15 @@ def _back_solve(h, g, m):
 
 
 def gmres(a_op, m_op, b, restart=30, rel_tol=1e-7, max_iters=500, variant="single_reduce",
-          orthogonalization="mgs", x0=None):
+          orthogonalization="mgs", x0=None, reject_checks=0):
     """Returns (x, dict(iterations, converged, history, true_residuals,
-    iteration_reductions, residual_reductions, restarts))."""
+    iteration_reductions, residual_reductions, restarts)).
+    reject_checks (test hook, mirrors libgdsw's GDSW_DEBUG_REJECT_CHECKS):
+    the first k true-residual confirmations count as failed."""
     b = np.ascontiguousarray(b, dtype=np.float64)
     x = np.zeros(b.size) if x0 is None else np.array(x0, dtype=np.float64)
     m_op = m_op or (lambda v: v)
-    st = dict(it=0, res=0, itr=0, restarts=0, history=[1.0], true=[])
+    st = dict(it=0, res=0, itr=0, restarts=0, history=[1.0], true=[], reject=reject_checks)
     if variant == "single_reduce":
         x, conv = _sr(a_op, m_op, b, x, restart, rel_tol, max_iters, st)
     else:
@@ -431,6 +433,13 @@ def gmres(a_op, m_op, b, restart=30, rel_tol=1e-7, max_iters=500, variant="singl
     return x, dict(iterations=st["it"], converged=conv, history=np.array(st["history"]),
                    true_residuals=st["true"], iteration_reductions=st["itr"],
                    residual_reductions=st["res"], restarts=st["restarts"])
+
+
+def _rejected(st) -> bool:
+    if st["reject"] > 0:
+        st["reject"] -= 1
+        return True
+    return False
 
 
 def _bnorm(b, x, beta, st):
@@ -486,7 +495,7 @@ def _sr(A, M, b, x, R, tol, maxit, st):
                     st["res"] += 1
                     tr = float(np.linalg.norm(b - A(xc)))
                     st["true"].append((st["it"], tr / denom))
-                    if tr / denom <= tol:
+                    if tr / denom <= tol and not _rejected(st):
                         return xc, True
                     if brk or st["it"] >= maxit:
                         return xc, False
@@ -554,7 +563,7 @@ def _classic(A, M, b, x, R, tol, maxit, orth, st):
                 st["res"] += 1
                 tr = float(np.linalg.norm(b - A(xc)))
                 st["true"].append((st["it"], tr / denom))
-                if tr / denom <= tol:
+                if tr / denom <= tol and not _rejected(st):
                     return xc, True
                 if brk or st["it"] >= maxit:
                     return xc, False

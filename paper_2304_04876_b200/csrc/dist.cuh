@@ -20,35 +20,36 @@ struct gdsw_dist {
   gdsw::DBuf<char> box;
   gdsw::PeerTable peers{};
   std::vector<char*> opened;
-  uint64_t seq[gdsw::CH_COUNT] = {0, 0, 0};
+  // per-channel sequence counters + CTA tickets on the device (graph-safe)
+  gdsw::DBuf<uint64_t> dseq;
+  gdsw::DBuf<unsigned> ddone;
   bool ready = false;
+  gdsw::SeqCounter counters() const { return gdsw::SeqCounter{dseq.p, ddone.p}; }
   gdsw::DBuf<double> red_in, red_out;  // scratch for reductions
   ~gdsw_dist() {
     for (size_t q = 0; q < opened.size(); ++q)
       if (opened[q] && (int)q != rank) cudaIpcCloseMemHandle(opened[q]);
   }
 
-  void allreduce(const double* d_in, double* d_out, int64_t m, cudaStream_t s) {
+  void allreduce(const double* d_in, double* d_out, int64_t m, cudaStream_t s, int ch = gdsw::CH_RED) {
     gdsw::require(ready, "distributed layout has no opened peers");
     gdsw::require(m <= layout.red_max, "reduction larger than the mailbox slot");
     if (nranks == 1) {
       if (d_in != d_out) CK(cudaMemcpyAsync(d_out, d_in, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
       return;
     }
-    const uint64_t sq = ++seq[gdsw::CH_RED];
-    gdsw::k_comm_allreduce<<<1, 256, 0, s>>>(peers, layout, rank, sq, d_in, d_out, m);
+    gdsw::k_comm_allreduce<<<1, 256, 0, s>>>(peers, layout, rank, counters(), ch, d_in, d_out, m);
     CK_LAUNCH();
   }
   void halo_fwd(double* x_ext, cudaStream_t s) {
     if (nranks == 1 || halo.nn == 0) return;
-    const uint64_t sq = ++seq[gdsw::CH_FWD];
-    gdsw::k_comm_halo_fwd<<<2 * halo.nn, 1024, 0, s>>>(peers, layout, halo, rank, sq, x_ext);
+    gdsw::k_comm_halo_fwd<<<2 * halo.nn, 1024, 0, s>>>(peers, layout, halo, rank, counters(), x_ext);
     CK_LAUNCH();
   }
   void halo_rev(const double* part_ext, double* recv_ext, cudaStream_t s) {
     if (nranks == 1 || halo.nn == 0) return;
-    const uint64_t sq = ++seq[gdsw::CH_REV];
-    gdsw::k_comm_halo_rev<<<2 * halo.nn, 1024, 0, s>>>(peers, layout, halo, rank, sq, part_ext, recv_ext);
+    gdsw::k_comm_halo_rev<<<2 * halo.nn, 1024, 0, s>>>(peers, layout, halo, rank, counters(), part_ext,
+                                                         recv_ext);
     CK_LAUNCH();
   }
 };

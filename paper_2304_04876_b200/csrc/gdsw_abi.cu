@@ -848,10 +848,10 @@ void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
     ProfScope ps("halo_fwd", s, 0.0);
     Dd->halo_fwd(const_cast<double*>(r), s);
   }
-  // the coarse restriction and solve only read r: on one GPU they run on
-  // the side stream, overlapped with the local solves, joined before the
-  // prolongation
-  const bool fork = Cp && !Dd && !env_flag("GDSW_NO_OVERLAP");
+  // the coarse restriction, the coarse right-hand side's all-reduce (sharded
+  // path) and the coarse solve only read r: they run on the side stream,
+  // overlapped with the local solves, joined before the prolongation
+  const bool fork = Cp && !env_flag("GDSW_NO_OVERLAP");
   cudaStream_t cs = s;
   if (fork) {
     CK(cudaEventRecord(m->ev_fork, s));
@@ -876,11 +876,12 @@ void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
     }
     if (Dd) {
       // coarse right-hand side: every rank's partial, summed in rank order
-      ProfScope ps("coarse_allreduce", s, 0.0);
-      k_cast_to_f64<T><<<grid_for(Cp->n_c, TB), TB, 0, s>>>(Cp->n_c, (const T*)m->cu.p, m->red64.p);
+      // (own channel: it runs on the side stream)
+      ProfScope ps("coarse_allreduce", cs, 0.0);
+      k_cast_to_f64<T><<<grid_for(Cp->n_c, TB), TB, 0, cs>>>(Cp->n_c, (const T*)m->cu.p, m->red64.p);
       CK_LAUNCH();
-      Dd->allreduce(m->red64.p, m->red64.p + Cp->n_c, Cp->n_c, s);
-      k_cast_from_f64<T><<<grid_for(Cp->n_c, TB), TB, 0, s>>>(Cp->n_c, m->red64.p + Cp->n_c, (T*)m->cu.p);
+      Dd->allreduce(m->red64.p, m->red64.p + Cp->n_c, Cp->n_c, cs, CH_CRS);
+      k_cast_from_f64<T><<<grid_for(Cp->n_c, TB), TB, 0, cs>>>(Cp->n_c, m->red64.p + Cp->n_c, (T*)m->cu.p);
       CK_LAUNCH();
     }
     ProfScope ps("coarse_solve", cs, (double)Cp->n_c * Cp->n_c * sizeof(T));
@@ -940,10 +941,11 @@ void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
 // join) replayed as a CUDA graph: captured on the second apply with the
 // same (r, z, stream) -- the first one runs eagerly and performs every lazy
 // allocation -- and dropped whenever the preconditioner's data changes.
-// Not used while the per-kernel profiler records events, on the sharded path
-// (its collectives spin on peers) or with GDSW_NO_GRAPH=1.
+// Not used while the per-kernel profiler records events or with
+// GDSW_NO_GRAPH=1. The sharded path's collectives take their sequence
+// numbers from device counters, so they replay inside graphs too.
 bool apply_graph_ok(const gdsw_precond* m) {
-  return !m->dist && !prof().on && !env_flag("GDSW_NO_GRAPH") && !env_flag("GDSW_NO_OVERLAP");
+  return !prof().on && !env_flag("GDSW_NO_GRAPH") && !env_flag("GDSW_NO_OVERLAP");
 }
 
 // the apply's launches enqueued into a stream that is being captured into a
@@ -1314,51 +1316,109 @@ __global__ void k_unit(int32_t n, int32_t c, double* __restrict__ v) {
   if (i < n) v[i] = i == c ? 1.0 : 0.0;
 }
 
-int gdsw_precond_coarse_galerkin(gdsw_precond* m, const gdsw_csr* a, double* a0_dense) {
-  return guarded([&] {
-    require(m->cp != nullptr && m->has_phi, "coarse basis is not set up");
-    require(a->dtype == GDSW_F64, "the Galerkin product reads the float64 operator values");
-    CoarsePlan* Cp = m->cp.get();
-    gdsw_plan* P = m->plan;
-    const int32_t nc = Cp->n_c;
-    const int64_t n = P->n;
-    // float64 Phi: panels (always kept in f64) + interface values
-    DBuf<double> pgr(std::max<size_t>(Cp->h_pgr_val.size(), 1)), pgt(std::max<size_t>(Cp->h_pgt_val.size(), 1));
-    if (!Cp->h_pgr_val.empty()) CK(cudaMemcpy(pgr.p, Cp->h_pgr_val.data(), Cp->h_pgr_val.size() * 8, cudaMemcpyHostToDevice));
-    if (!Cp->h_pgt_val.empty()) CK(cudaMemcpy(pgt.p, Cp->h_pgt_val.data(), Cp->h_pgt_val.size() * 8, cudaMemcpyHostToDevice));
-    DBuf<double> v(std::max(nc, 1)), z(std::max<int64_t>(n, 1)), y(std::max<int64_t>(n, 1)),
-        zero_loc(std::max<int64_t>(P->n_loc, 1)), part(std::max<int64_t>(Cp->n_partial, 1)),
-        a0((size_t)std::max(nc, 1) * std::max(nc, 1));
-    zero_loc.zero();
-    const ChunkDev D = Cp->chunk_dev();
-    const int32_t nblk = Cp->n_chunks + (int32_t)((Cp->n_gamma + CH_THREADS - 1) / CH_THREADS);
-    // column c of A0 = Phi^T (A (Phi e_c)): the apply's own prolongation,
-    // SpMV and restriction kernels in float64
+// A0 = Phi^T A Phi column by column with the apply's own float64
+// prolongation, SpMV and restriction kernels (the reference's coarse_matrix,
+// coarse_space.py:205-207). Sharded (d != null): Phi e_c on my rows, its halo
+// from the owners, A on my owned rows, my rows' share of Phi^T, then the
+// partial A0 summed over ranks in rank order through the peer-memory
+// all-reduce -- identical on every rank, no host round trip.
+__global__ void k_abs_copy(int64_t n, const double* __restrict__ x, double* __restrict__ y) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] = fabs(x[i]);
+}
+
+DBuf<double> abs_copy(const double* x, size_t n) {
+  DBuf<double> y(std::max<size_t>(n, 1));
+  if (n) {
+    k_abs_copy<<<grid_for((int64_t)n, TB), TB>>>((int64_t)n, x, y.p);
+    CK_LAUNCH();
+  }
+  return y;
+}
+
+// pattern != null: also the structural pattern of Phi^T A Phi -- the same
+// product over |Phi| and |A| (no cancellation), nonzero exactly where the
+// reference's Gustavson SpGEMM creates an entry, computed zeros included
+// (coarse_space.py:205-207, _kernels.py:51-94)
+static void coarse_galerkin(gdsw_precond* m, const gdsw_csr* a, gdsw_dist* d, double* a0_dense,
+                            uint8_t* pattern = nullptr) {
+  require(m->cp != nullptr && m->has_phi, "coarse basis is not set up");
+  require(a->dtype == GDSW_F64, "the Galerkin product reads the float64 operator values");
+  CoarsePlan* Cp = m->cp.get();
+  gdsw_plan* P = m->plan;
+  const int32_t nc = Cp->n_c;
+  const int64_t n = P->n;
+  const int64_t off = d ? d->own_off : 0;
+  if (d) require(d->ready && d->n_ext == n && a->nrows == d->n_own && a->ncols == n,
+                 "layout does not match the preconditioner");
+  // float64 Phi: panels (always kept in f64) + interface values
+  DBuf<double> pgr(std::max<size_t>(Cp->h_pgr_val.size(), 1)), pgt(std::max<size_t>(Cp->h_pgt_val.size(), 1));
+  if (!Cp->h_pgr_val.empty()) CK(cudaMemcpy(pgr.p, Cp->h_pgr_val.data(), Cp->h_pgr_val.size() * 8, cudaMemcpyHostToDevice));
+  if (!Cp->h_pgt_val.empty()) CK(cudaMemcpy(pgt.p, Cp->h_pgt_val.data(), Cp->h_pgt_val.size() * 8, cudaMemcpyHostToDevice));
+  DBuf<double> v(std::max(nc, 1)), z(std::max<int64_t>(n, 1)), y(std::max<int64_t>(n, 1)),
+      zero_loc(std::max<int64_t>(P->n_loc, 1)), part(std::max<int64_t>(Cp->n_partial, 1)),
+      a0((size_t)std::max(nc, 1) * std::max(nc, 1));
+  zero_loc.zero();
+  z.zero();
+  const ChunkDev D = Cp->chunk_dev();
+  const int32_t nblk = Cp->n_chunks + (int32_t)((Cp->n_gamma + CH_THREADS - 1) / CH_THREADS);
+  // one pass: A0 (or, over absolute values, its structural pattern)
+  auto product = [&](const double* panel, const double* pgr_v, const double* pgt_v, const double* aval,
+                     DBuf<double>& out) {
     for (int32_t c = 0; c < nc; ++c) {
       k_unit<<<grid_for(nc, TB), TB>>>(nc, c, v.p);
       CK_LAUNCH();
       if (nblk > 0) {
-        k_prolong<double><<<nblk, CH_THREADS>>>(Cp->n_chunks, D, m->panel64.p,
+        k_prolong<double><<<nblk, CH_THREADS>>>(Cp->n_chunks, D, panel,
                                                ProlongGamma{(int32_t)Cp->n_gamma, Cp->gamma32.p, Cp->pgam_ptr.p,
                                                             Cp->pgam_col.p},
-                                               pgr.p, v.p, P->sc_ptr.p, P->sc_pos.p, zero_loc.p, RemoteAdd{}, z.p);
+                                               pgr_v, v.p, P->sc_ptr.p, P->sc_pos.p, zero_loc.p, RemoteAdd{}, z.p);
         CK_LAUNCH();
       }
-      spmv_T<double>(a, z.p, nullptr, y.p, 0, 1.0, 0.0, 0);
+      if (d) d->halo_fwd(z.p, 0);
+      if (a->nrows > 0) {
+        if (a->pat.has16)
+          k_sell_spmv<double, true><<<grid_for(a->nrows, TB), TB>>>(a->pat.view(), aval, z.p, nullptr, y.p + off,
+                                                                   0, 1.0, 0.0);
+        else
+          k_sell_spmv<double, false><<<grid_for(a->nrows, TB), TB>>>(a->pat.view(), aval, z.p, nullptr, y.p + off,
+                                                                    0, 1.0, 0.0);
+        CK_LAUNCH();
+      }
       if (Cp->n_chunks > 0) {
-        k_restrict_chunks<double><<<Cp->n_chunks, RS_THREADS>>>(D, m->panel64.p, y.p, part.p);
+        k_restrict_chunks<double><<<Cp->n_chunks, RS_THREADS>>>(D, panel, y.p, part.p);
         CK_LAUNCH();
       }
-      k_restrict_columns<double><<<nc, 256>>>(nc, Cp->pgt_ptr.p, Cp->pgt_row.p, pgt.p, y.p, Cp->cpart_ptr.p,
-                                              Cp->cpart_idx.p, part.p, a0.p + (size_t)c * nc);
+      k_restrict_columns<double><<<nc, 256>>>(nc, Cp->pgt_ptr.p, Cp->pgt_row.p, pgt_v, y.p, Cp->cpart_ptr.p,
+                                              Cp->cpart_idx.p, part.p, out.p + (size_t)c * nc);
       CK_LAUNCH();
     }
+    if (d && d->nranks > 1) {
+      const int64_t total = (int64_t)nc * nc, step = d->layout.red_max;
+      for (int64_t o = 0; o < total; o += step)
+        d->allreduce(out.p + o, out.p + o, std::min(step, total - o), 0);
+    }
+  };
+  product(m->panel64.p, pgr.p, pgt.p, (const double*)a->sell_val.p, a0);
+  CK(cudaDeviceSynchronize());
+  // a0 holds columns contiguously: transpose into the row-major output
+  std::vector<double> h = a0.download();
+  for (int32_t c = 0; c < nc; ++c)
+    for (int32_t r = 0; r < nc; ++r) a0_dense[(size_t)r * nc + c] = h[(size_t)c * nc + r];
+  if (pattern) {
+    DBuf<double> pan_a = abs_copy(m->panel64.p, Cp->panel_entries), pgr_a = abs_copy(pgr.p, Cp->h_pgr_val.size()),
+                 pgt_a = abs_copy(pgt.p, Cp->h_pgt_val.size()),
+                 a_a = abs_copy((const double*)a->sell_val.p, a->sell_val.n / sizeof(double));
+    product(pan_a.p, pgr_a.p, pgt_a.p, a_a.p, a0);
     CK(cudaDeviceSynchronize());
-    // a0 holds columns contiguously: transpose into the row-major output
-    std::vector<double> h = a0.download();
+    h = a0.download();
     for (int32_t c = 0; c < nc; ++c)
-      for (int32_t r = 0; r < nc; ++r) a0_dense[(size_t)r * nc + c] = h[(size_t)c * nc + r];
-  });
+      for (int32_t r = 0; r < nc; ++r) pattern[(size_t)r * nc + c] = h[(size_t)c * nc + r] != 0.0;
+  }
+}
+
+int gdsw_precond_coarse_galerkin(gdsw_precond* m, const gdsw_csr* a, double* a0_dense, uint8_t* pattern) {
+  return guarded([&] { coarse_galerkin(m, a, nullptr, a0_dense, pattern); });
 }
 
 int gdsw_precond_set_coarse_inverse(gdsw_precond* m, const double* a0inv) {

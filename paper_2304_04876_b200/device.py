@@ -66,7 +66,9 @@ _SIGS = {
     "gdsw_precond_get_factors": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "gdsw_plan_set_block_pattern": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "gdsw_precond_lu_numeric": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p]),
-    "gdsw_precond_coarse_galerkin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gdsw_precond_coarse_galerkin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "gdsw_dist_coarse_galerkin": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                             C.c_void_p]),
     "gdsw_sr_update": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "gdsw_precond_extend": (C.c_int, [C.c_void_p, C.c_void_p, C.c_double, C.c_int, C.c_void_p,
@@ -326,11 +328,23 @@ class Precond:
         _ck(_lib.gdsw_precond_lu_numeric(self.handle, a_dev.handle, float(diag_shift), _ptr(fail)))
         return fail[:n_sub]
 
-    def coarse_galerkin(self, a_dev: DeviceCsr, n_c: int) -> np.ndarray:
-        """Dense A0 = Phi^T A Phi (float64) from the device coarse basis."""
+    def coarse_galerkin(self, a_dev: DeviceCsr, n_c: int, layout=None):
+        """A0 = Phi^T A Phi (float64) from the device coarse basis, as a
+        CsrMatrix with the reference's SpGEMM pattern (computed zeros kept).
+        layout: the rank's DistLayout on the sharded path (a_dev = its owned
+        rows); the partial products are summed over ranks on the device."""
+        from .sparse_core import CsrMatrix
         out = np.zeros((n_c, n_c), dtype=np.float64)
-        _ck(_lib.gdsw_precond_coarse_galerkin(self.handle, a_dev.handle, _ptr(out)))
-        return out
+        pat = np.zeros((n_c, n_c), dtype=np.uint8)
+        if layout is None:
+            _ck(_lib.gdsw_precond_coarse_galerkin(self.handle, a_dev.handle, _ptr(out), _ptr(pat)))
+        else:
+            _ck(_lib.gdsw_dist_coarse_galerkin(self.handle, a_dev.handle, layout.handle, _ptr(out),
+                                               _ptr(pat)))
+        rows, cols = np.nonzero(pat)
+        ptr = np.zeros(n_c + 1, dtype=np.int64)
+        np.add.at(ptr, rows + 1, 1)
+        return CsrMatrix(n_c, n_c, np.cumsum(ptr), cols.astype(np.int64), out[rows, cols])
 
     def factors(self, nnz_l: int, nnz_u: int):
         lv = np.empty(nnz_l, dtype=self.value_dtype)

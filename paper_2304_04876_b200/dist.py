@@ -32,8 +32,8 @@ from .coarse_space import (
     interior_sets,
 )
 from .local_solvers import LocalFactorization, build_symbolic, host_numeric, make_ordering
-from .local_solvers import numeric_lu, symbolic_lu
-from .sparse_core import CsrMatrix, convert_precision, extract_submatrix, spgemm, transpose
+from .local_solvers import _pivot_error, numeric_lu, symbolic_lu
+from .sparse_core import CsrMatrix, convert_precision, extract_submatrix
 
 
 @dataclass
@@ -126,6 +126,7 @@ class DistPreconditioner:
         import torch.distributed as tdist
 
         from . import device
+        from .schwarz import _gpu_lu_pays
         self.shard = sh = shard
         spec = config.local
         single = config.precision == "single"
@@ -157,6 +158,16 @@ class DistPreconditioner:
         a_ext_dev = device.DeviceCsr(a_ext)
         if spec.method == "fast_ilu":
             self.sweep_residuals = self.pre.fastilu(a_ext_dev, spec.factor_sweeps, len(sets))
+        elif self.plan.has_block_pattern and _gpu_lu_pays(spec, syms):
+            # the single-GPU numeric LU / ILU(k) kernel on this rank's blocks
+            shift = spec.diag_shift if spec.method == "ilu_k" else 0.0
+            fail = self.pre.lu_numeric(a_ext_dev, shift, len(sets))
+            bad = np.flatnonzero(fail)
+            if bad.size:
+                i = int(bad[0])
+                err = _pivot_error(syms[i], int(fail[i]))
+                raise np.linalg.LinAlgError(
+                    f"local matrix of subdomain {int(sh.subs[i])} failed to factor: {err}")
         else:
             lvs, uvs = [], []
             shift = spec.diag_shift if spec.method == "ilu_k" else 0.0
@@ -179,8 +190,6 @@ class DistPreconditioner:
         self.a_own = device.DeviceCsr(extract_submatrix(a, own, ext))
 
     def _coarse(self, a, coarse_src, a_ext, a_ext_dev, dec, nullspace, config, single, group):
-        import torch
-        import torch.distributed as tdist
         sh = self.shard
         structure = dec.structure
         basis = interface_basis(nullspace, structure)
@@ -226,17 +235,12 @@ class DistPreconditioner:
             phi_ext = CsrMatrix.from_coo(sh.n_ext, n_c, r1, c1, v1)
         else:
             phi_ext = phi_own
+        # A0 = Phi^T A Phi on the GPU: my owned rows' share, summed over ranks
+        # in rank order by the peer-memory all-reduce (identical everywhere)
         own = _range_rows(sh.g0, sh.g1)
-        a_own = extract_submatrix(coarse_src, own, _range_rows(sh.e0, sh.e1))
-        w = spgemm(a_own, phi_ext)
-        phi_rows = extract_submatrix(phi_ext, own - sh.e0, np.arange(n_c))
-        part = spgemm(transpose(phi_rows), w).to_dense()
-        parts = [None] * sh.nranks
-        tdist.all_gather_object(parts, part, group=group)
-        a0d = np.zeros((n_c, n_c))
-        for p in parts:                 # rank order: identical on every rank
-            a0d = a0d + p
-        a0 = CsrMatrix.from_dense(a0d)
+        from . import device
+        a_own_src = device.DeviceCsr(extract_submatrix(coarse_src, own, _range_rows(sh.e0, sh.e1)))
+        a0 = self.pre.coarse_galerkin(a_own_src, n_c, self.layout)
         if single:
             a0 = convert_precision(a0, np.float32)
         try:
@@ -248,7 +252,6 @@ class DistPreconditioner:
         self.phi_local = phi_ext
         self.column_map = column_map
         self.coarse_n = n_c
-        del torch
 
     def solve(self, b_own, cfg, x0_own=None):
         """Sharded native GMRES on device vectors of this rank's owned rows."""

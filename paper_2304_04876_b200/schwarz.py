@@ -482,10 +482,9 @@ def setup_numeric(skeleton: PreconditionerSkeleton, a: CsrMatrix,
         basis = interface_basis(nullspace, structure)
         phi64, column_map, _ = extend_on_device(pre, a_src_dev, coarse_src, structure, basis,
                                                 skeleton.interior_sets, lazy_phi=True)
-        # A0 = Phi^T A Phi on the GPU from the float64 panels (the reference's
-        # coarse_matrix, coarse_space.py:205-207; exact zeros of the dense
-        # product are not kept as entries)
-        a0 = CsrMatrix.from_dense(pre.coarse_galerkin(a_src_dev, len(column_map)))
+        # A0 = Phi^T A Phi on the GPU from the float64 panels, with the
+        # reference's SpGEMM pattern (coarse_matrix, coarse_space.py:205-207)
+        a0 = pre.coarse_galerkin(a_src_dev, len(column_map))
         phi = phi64
         if single:
             phi = lambda: convert_precision(phi64(), np.float32)  # noqa: E731

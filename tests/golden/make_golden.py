@@ -51,6 +51,8 @@ def one(name, case):
     if pre.coarse is not None:
         arrays["phi_dense"] = pre.coarse.phi.to_dense()
         arrays["a0_dense"] = pre.coarse.a0.to_dense()
+        arrays["a0_row_ptr"] = pre.coarse.a0.row_ptr
+        arrays["a0_col_idx"] = pre.coarse.a0.col_idx
         out["n_coarse"] = pre.coarse.a0.nrows
     x_star, b = rhs(prob)
     for variant, orth in (("single_reduce", "mgs"), ("classic", "mgs"), ("classic_cgs2", "cgs2")):

@@ -63,15 +63,24 @@ def _rank_main(rank, world, port, method, q):
         b = prob.a @ np.random.default_rng(0).standard_normal(prob.a.nrows)
         bo = torch.from_numpy(b[sh.g0:sh.g1].copy()).cuda()
         x, rep = pre.solve(bo, KrylovConfig(variant="single_reduce"))
+        x, rep = pre.solve(bo, KrylovConfig(variant="single_reduce"))   # replayed pass graphs
+        os.environ["GDSW_NO_GRAPH"] = "1"
+        xe, _ = pre.solve(bo, KrylovConfig(variant="single_reduce"))
+        del os.environ["GDSW_NO_GRAPH"]
         torch.cuda.synchronize()
+        graph_ok = bool(torch.equal(x, xe))
         q.put((rank, red_ok, halo_ok, sh.g0, x.cpu().numpy(), rep["iterations"], rep["converged"],
-               list(rep["history"])))
+               list(rep["history"]), graph_ok, pre.a0.to_dense().astype(np.float64),
+               pre.a0.row_ptr.copy(), pre.a0.col_idx.copy()))
     finally:
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("method", ["fast_ilu", "ilu_k"])
+@pytest.mark.parametrize("method", ["fast_ilu", "ilu_k", "exact_lu"])
 def test_sharded_gmres_two_ranks_one_gpu(method):
+    """Sharded solve (GPU numeric LU / FastILU per rank, GPU Galerkin A0 summed
+    over ranks on the device, graphed passes with device-sequenced
+    collectives, the coarse side stream) == the single-GPU solve."""
     import torch.multiprocessing as mp
 
     from paper_2304_04876_b200.decomposition import decompose
@@ -105,4 +114,10 @@ def test_sharded_gmres_two_ranks_one_gpu(method):
     assert abs(res[0][5] - rep1.iterations) <= 1
     assert np.allclose(res[0][7][:5], rep1.residual_history[:5], rtol=1e-8)
     assert np.abs(xs - x1).max() <= 1e-6 * np.abs(x1).max()
+    assert all(r[8] for r in res), "graphed sharded passes == eager, bitwise"
+    a0 = pre.coarse.a0
+    for r in res:   # every rank: the single-GPU A0 (values; the reference's SpGEMM pattern)
+        assert np.array_equal(r[10], a0.row_ptr) and np.array_equal(r[11], a0.col_idx)
+        assert np.abs(r[9] - a0.to_dense()).max() <= 1e-12 * np.abs(a0.to_dense()).max()
+    assert np.array_equal(res[0][9], res[1][9])
     assert np.linalg.norm(b - prob.a @ xs) <= 1e-7 * np.linalg.norm(b) * 1.0001
