@@ -32,6 +32,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -47,7 +48,6 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "GDSW-GMRES solve s & iters to 1e-7, 3D Laplace 2M dof/GPU; apply HBM GB/s"
 # iterations of the reference on C2 (measured by running it)
-REFERENCE_ITERATIONS = {(128, 4, "fast_ilu(0,3,5)", "natural", "double"): 82}
 APPLY_PHASES = ("restrict_panels", "restrict_columns", "coarse_solve", "gather",
                 "gather_jacobi_lower", "jacobi_lower", "jacobi_lower_diag", "diag_solve", "jacobi_upper", "jacobi_flow", "levelset",
                 "prolong", "scatter")
@@ -70,6 +70,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--cpu-sample-iters", type=int, default=5)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--ref-budget", type=float, default=150.0,
+                   help="--impl reference: seconds of timed full solves (at least one)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--sharded", action="store_true",
                    help="run the sharded (multi-GPU) code path even at one rank")
@@ -433,73 +435,93 @@ def _oracle_sample(ore, prob, b, sample_iters: int):
 
 
 def cpu_baseline(args, prob, dec, cfg, skel, pre, b, iterations):
-    """Oracle port, 1 thread, BLAS pinned to 1 thread, on a bounded sample of
-    the same solve (the preconditioner's coarse basis taken from the GPU
-    setup; local factors from the oracle's own FastILU)."""
+    """Oracle port on 1 core (subdomain solves and BLAS on one thread): ONE
+    full solve of the same system from x0 = 0 to rtol 1e-7 (the coarse basis
+    taken from the GPU setup, local factors from the oracle's own FastILU)."""
     from oracle import oracle as O
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
     try:
         from threadpoolctl import threadpool_limits
         limiter = threadpool_limits(1)
     except Exception:
         limiter = None
-    ore = O.OracleSchwarz(prob.a, dec, cfg, None, symbolics=skel.local_symbolics,
-                          threads=os.cpu_count() or 1,
+    ore = O.OracleSchwarz(prob.a, dec, cfg, None, symbolics=skel.local_symbolics, threads=1,
                           coarse_parts=(pre.coarse.phi, pre.coarse.a0))
-    per_it = _oracle_sample(ore, prob, b, args.cpu_sample_iters)
-    if limiter is not None:
-        limiter.unregister() if hasattr(limiter, "unregister") else None
-    return {"value": per_it * iterations, "unit": "s", "cores": 1, "kind": "port",
-            "per_iteration_s": per_it,
-            "sample": f"oracle single-reduce GMRES, {args.cpu_sample_iters} iterations of the "
-                      f"C2 solve on 1 core (BLAS 1 thread), per-iteration time x {iterations} "
-                      "iterations; oracle FastILU factors, coarse basis from the GPU setup"}
+    t0 = time.perf_counter()
+    _, rep = O.gmres(lambda v: O.csr_spmv(prob.a, v), ore.apply, b)
+    value = time.perf_counter() - t0
+    if limiter is not None and hasattr(limiter, "unregister"):
+        limiter.unregister()
+    return {"value": value, "unit": "s", "cores": 1, "kind": "port",
+            "per_iteration_s": value / max(rep["iterations"], 1), "iterations": rep["iterations"],
+            "cpu_model": cpu_model(),
+            "sample": f"one full oracle single-reduce GMRES solve of the same system on 1 core "
+                      f"(BLAS 1 thread): {rep['iterations']} iterations (GPU {iterations}); "
+                      "oracle FastILU factors, coarse basis from the GPU setup"}
+
+
+def cpu_model() -> str:
+    """`lscpu`'s model name (BASELINE.md section 2 asks for it)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
 
 
 def reference(args):
     """The reference's CPU implementation of the path (oracle port) on this
-    host: full CPU setup (FastILU, exact-LU harmonic extension), then bounded
-    GMRES samples of the same solve."""
+    host: full CPU setup (FastILU, exact-LU harmonic extension), then FULL
+    GMRES solves of the same system (x0 = 0 to rtol 1e-7), subdomain solves
+    and BLAS on every host thread. Warm-up steps are short samples; the timed
+    steps are whole solves, as many of the K requested as fit the time budget
+    (--ref-budget seconds, at least one)."""
     world, rank, _ = dist_setup()
     if rank != 0:
         return
     from oracle import oracle as O
     cores = os.cpu_count() or 1
+    try:  # numpy BLAS (GMRES vector work) on every host thread as well
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(cores)
+    except Exception:
+        pass
     prob, dec, cfg = build_problem(args)
     t0 = time.perf_counter()
     ore = O.OracleSchwarz(prob.a, dec, cfg, prob.nullspace, threads=cores)
     t_setup = time.perf_counter() - t0
     x_star = np.random.default_rng(0).standard_normal(prob.a.nrows)
     b = prob.a @ x_star
-    key = (args.n, args.parts, args.solver, args.ordering, args.precision)
-    iters = REFERENCE_ITERATIONS.get(key)
-    if iters is None:
-        _, rep = O.gmres(lambda v: O.csr_spmv(prob.a, v), ore.apply, b)
-        iters = rep["iterations"]
-    try:  # numpy BLAS (GMRES vector work) on every host thread as well
-        from threadpoolctl import threadpool_limits
-        threadpool_limits(cores)
-    except Exception:
-        pass
     for _ in range(args.warmup):
         _oracle_sample(ore, prob, b, args.cpu_sample_iters)
-    per = [_oracle_sample(ore, prob, b, args.cpu_sample_iters) for _ in range(args.steps)]
-    per_it = float(np.mean(per))
-    value = per_it * iters
+    times, iters, true_rel = [], None, None
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        t1 = time.perf_counter()
+        x, rep = O.gmres(lambda v: O.csr_spmv(prob.a, v), ore.apply, b)
+        times.append(time.perf_counter() - t1)
+        iters = rep["iterations"]
+        if time.perf_counter() - t_all + times[-1] > args.ref_budget:
+            break
+    true_rel = float(np.linalg.norm(b - prob.a @ x) / np.linalg.norm(b))
+    value = float(np.mean(times))
     sample = (f"oracle port of the reference path (plain-C sequential kernels + numpy "
-              f"single-reduce GMRES), each step {args.cpu_sample_iters} GMRES iterations of "
-              f"the C2 solve with subdomain solves on {cores} threads (the reference's "
-              f"`threads` option) and BLAS on {cores} threads, per-iteration time x {iters} "
-              f"iterations (the reference's count on C2); setup {t_setup:.1f}s not timed")
+              f"single-reduce GMRES): {len(times)} full solve(s) of the {workload(args)['workload']} "
+              f"system from x0 = 0 to rtol 1e-7 ({iters} iterations, true relative residual "
+              f"{true_rel:.2e}), subdomain solves on {cores} threads (the reference's `threads` "
+              f"option) and BLAS on {cores} threads; {args.warmup} warm-up samples of "
+              f"{args.cpu_sample_iters} iterations; setup {t_setup:.1f}s not timed")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * per_it *
-        args.cpu_sample_iters, "higher_is_better": False, "scaling": "weak",
+        "steps": len(times), "steps_requested": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * value, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference generators, x*=default_rng(0).standard_normal(n), b=A x*",
-        "config": workload(args), "iterations": iters, "ms_per_iteration": 1e3 * per_it,
+        "config": workload(args), "iterations": iters, "ms_per_iteration": 1e3 * value / iters,
+        "true_relative_residual": true_rel,
         "cpu_baseline": {"value": value, "unit": "s", "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
