@@ -1,0 +1,261 @@
+"""Factored coarse solve for large coarse spaces (schwarz.py:267-272, 305).
+
+The reference keeps a sparse LU of A0 (ordering = config.ordering) and runs
+level-set triangular solves on it every apply. A dense A0^-1 GEMV reads
+n_c^2 values per apply (1.27 GB at n_c = 12,600), and a level-set solve of
+the sparse factors is a chain of ~3,000 one-row levels; neither scales. The
+B200 path uses a supernodal PARTITIONED INVERSE of the nested-dissection LU:
+
+* A0 is permuted by nested dissection and factored without pivoting
+  (A0 = L U, the reference's pivot-free factorization; dense on the device
+  at setup, cuSOLVER through torch, so nothing O(n_c^3) runs on the host).
+* Columns are grouped into supernodes (fundamental supernodes, then
+  single-child chains amalgamated when the explicit zeros stay bounded),
+  each with its column set C_k (s_k columns) and the rows R_k below it.
+* Forward solve, one kernel per supernode-tree level (leaves first): with
+  bt_k = b[C_k] - (contributions of descendants), the level computes
+  [y_k; c_k] = [L_kk^-1; L_{R_k,k} L_kk^-1] bt_k -- one dense GEMV per
+  supernode (no sequential substitution inside it); c_k is written to a
+  contribution buffer that the ancestors owning R_k gather in a fixed order.
+* Backward solve, one kernel per level (root first):
+  x_k = [U_kk^-1 | -U_kk^-1 U_{k,R_k}] [y_k; x[R_k]].
+
+Every level is a batch of bandwidth-parallel dense GEMVs; the byte count is
+nnz(L) + nnz(U) of the supernodal factors (7.8x less than the dense inverse
+at n_c = 12,600), and the number of launches is twice the supernode-tree
+height. Deterministic: fixed task decomposition, fixed reduction orders.
+The result is A0^-1 u to a few ulps times cond(A0) (compared with the dense
+inverse at 1e-12 in the tests; the reference's own LU solve is matched
+through the apply at 1e-10).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass
+class CoarseFactor:
+    """Host description of the supernodal partitioned inverse (all indices
+    are ORIGINAL coarse-column indices; values float64)."""
+    n: int
+    level_ptr: np.ndarray      # [n_levels + 1] ranges of supernodes, leaves first
+    sn_s: np.ndarray           # [n_sn] columns per supernode
+    sn_r: np.ndarray           # [n_sn] rows below
+    col_ptr: np.ndarray        # [n_sn + 1] into col_ids
+    col_ids: np.ndarray        # columns of each supernode (ascending ND position)
+    row_ptr: np.ndarray        # [n_sn + 1] into row_ids (== contribution buffer offsets)
+    row_ids: np.ndarray        # R_k of each supernode (ascending ND position)
+    d_off: np.ndarray          # [n_sn] offset of the s x s diagonal block (strict lower: L^-1, upper: U^-1)
+    m_off: np.ndarray          # [n_sn] offset of M_k = L_Rk L_kk^-1   (r x s, row-major)
+    n_off: np.ndarray          # [n_sn] offset of N_k = U_kk^-1 U_kR   (s x r, row-major)
+    values: np.ndarray         # float64
+    g_ptr: np.ndarray          # [n + 1] by original column: contribution slots to subtract
+    g_idx: np.ndarray          # contribution buffer positions, ascending supernode order
+
+    @property
+    def n_levels(self) -> int:
+        return self.level_ptr.size - 1
+
+    @property
+    def n_sn(self) -> int:
+        return self.sn_s.size
+
+
+def _lu_nopivot(a: np.ndarray) -> np.ndarray:
+    """Dense LU without pivoting (unit L strictly below, U on and above)."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            t = torch.from_numpy(a).cuda()
+            lu, _ = torch.linalg.lu_factor(t, pivot=False)
+            return lu.cpu().numpy()
+    except ImportError:  # pragma: no cover
+        pass
+    import scipy.linalg as sl
+    lu = np.array(a, dtype=np.float64, order="C", copy=True)
+    n = lu.shape[0]
+    nb = 128
+    for k0 in range(0, n, nb):
+        k1 = min(n, k0 + nb)
+        d = lu[k0:k1, k0:k1]
+        for k in range(k1 - k0):  # unblocked panel
+            piv = d[k, k]
+            d[k + 1:, k] /= piv
+            d[k + 1:, k + 1:] -= np.outer(d[k + 1:, k], d[k, k + 1:])
+        if k1 < n:
+            lkk = np.tril(d, -1) + np.eye(k1 - k0)
+            ukk = np.triu(d)
+            lu[k0:k1, k1:] = sl.solve_triangular(lkk, lu[k0:k1, k1:], lower=True, unit_diagonal=True)
+            lu[k1:, k0:k1] = sl.solve_triangular(ukk.T, lu[k1:, k0:k1].T, lower=True).T
+            lu[k1:, k1:] -= lu[k1:, k0:k1] @ lu[k0:k1, k1:]
+    return lu
+
+
+def _supernodes(nz: np.ndarray, max_zero_frac: float):
+    """Fundamental supernodes of the column structure `nz` (strictly lower,
+    symmetrized), then single-child chains merged while the dense blocks'
+    explicit zeros stay under `max_zero_frac`. Returns (starts, parent_of_sn)."""
+    n = nz.shape[0]
+    cc = nz.sum(axis=0)
+    parent = np.full(n, -1, dtype=np.int64)
+    for j in range(n):
+        r = np.flatnonzero(nz[j + 1:, j])
+        if r.size:
+            parent[j] = j + 1 + r[0]
+    nchild = np.bincount(parent[parent >= 0], minlength=n)
+    starts = [0]
+    for j in range(1, n):
+        fund = parent[j - 1] == j and cc[j - 1] == cc[j] + 1 and nchild[j] == 1
+        if not fund:
+            starts.append(j)
+    starts = np.asarray(starts + [n], dtype=np.int64)
+    # amalgamate: supernode k merges into its parent when it is the parent's
+    # only child and directly precedes it (postorder) and the merged dense
+    # block keeps the explicit zeros bounded
+    changed = True
+    while changed:
+        changed = False
+        sn_of = np.repeat(np.arange(starts.size - 1), np.diff(starts))
+        nsn = starts.size - 1
+        sp = np.full(nsn, -1, dtype=np.int64)
+        for k in range(nsn):
+            p = parent[starts[k + 1] - 1]
+            if p >= 0:
+                sp[k] = sn_of[p]
+        nch = np.bincount(sp[sp >= 0], minlength=nsn)
+        keep = np.ones(nsn + 1, dtype=bool)
+        k = 0
+        while k < nsn:
+            p = sp[k]
+            if p == k + 1 and nch[p] == 1:
+                c0, c1, p1 = starts[k], starts[k + 1], starts[p + 1]
+                rows_c = np.flatnonzero(nz[c1:, c0:c1].any(axis=1)) + c1
+                rows_p = np.flatnonzero(nz[p1:, c1:p1].any(axis=1)) + p1
+                rows = np.union1d(rows_c[rows_c >= p1], rows_p)
+                s = p1 - c0
+                dense = s * s + 2 * s * rows.size
+                actual = (np.count_nonzero(nz[c0:p1, c0:p1]) * 2 + s +
+                          2 * np.count_nonzero(nz[rows][:, c0:p1]))
+                if dense and 1.0 - actual / dense <= max_zero_frac:
+                    keep[k + 1] = False
+                    changed = True
+                    k += 2
+                    continue
+            k += 1
+        starts = starts[keep]
+    return starts, parent
+
+
+def build_coarse_factor(a0, perm: np.ndarray | None = None,
+                        max_zero_frac: float = 0.3) -> CoarseFactor:
+    """Supernodal partitioned inverse of A0 (CsrMatrix or dense ndarray)."""
+    from .local_solvers import make_ordering
+    dense = a0 if isinstance(a0, np.ndarray) else a0.to_dense()
+    dense = np.asarray(dense, dtype=np.float64)
+    n = dense.shape[0]
+    if perm is None:
+        perm = make_ordering(a0, "nested_dissection").perm
+    perm = np.asarray(perm, dtype=np.int64)
+    ap = np.ascontiguousarray(dense[np.ix_(perm, perm)])
+    lu = _lu_nopivot(ap)
+    if not np.all(np.isfinite(lu)) or np.any(np.diag(lu) == 0.0):
+        raise np.linalg.LinAlgError("coarse matrix is singular")
+    low = np.tril(lu, -1)
+    up = np.triu(lu, 1)
+    nz = (low != 0.0) | (up.T != 0.0)
+    del low, up
+    starts, _ = _supernodes(nz, max_zero_frac)
+    nsn = starts.size - 1
+    sn_of = np.repeat(np.arange(nsn), np.diff(starts))
+    # supernode tree and levels (height from the leaves)
+    sn_rows = []
+    sn_par = np.full(nsn, -1, dtype=np.int64)
+    for k in range(nsn):
+        c0, c1 = starts[k], starts[k + 1]
+        rows = np.flatnonzero(nz[c1:, c0:c1].any(axis=1)) + c1
+        sn_rows.append(rows)
+        if rows.size:
+            sn_par[k] = sn_of[rows[0]]
+    height = np.zeros(nsn, dtype=np.int64)
+    for k in range(nsn):  # children precede parents (ND postorder)
+        if sn_par[k] >= 0:
+            height[sn_par[k]] = max(height[sn_par[k]], height[k] + 1)
+    order = np.lexsort((np.arange(nsn), height))
+    level_ptr = np.searchsorted(height[order], np.arange(height.max() + 2)).astype(np.int64)
+    import scipy.linalg as sl
+    vals, d_off, m_off, n_off = [], [], [], []
+    col_ids, row_ids = [], []
+    sn_s = np.zeros(nsn, dtype=np.int64)
+    sn_r = np.zeros(nsn, dtype=np.int64)
+    off = 0
+    for q, k in enumerate(order):
+        c0, c1 = starts[k], starts[k + 1]
+        rows = sn_rows[k]
+        s, r = c1 - c0, rows.size
+        sn_s[q], sn_r[q] = s, r
+        blk = lu[c0:c1, c0:c1]
+        lkk = np.tril(blk, -1) + np.eye(s)
+        ukk = np.triu(blk)
+        linv = sl.solve_triangular(lkk, np.eye(s), lower=True, unit_diagonal=True)
+        uinv = sl.solve_triangular(ukk, np.eye(s), lower=False)
+        dblk = np.tril(linv, -1) + np.triu(uinv)
+        mk = lu[np.ix_(rows, np.arange(c0, c1))] @ linv if r else np.zeros((0, s))
+        nk = uinv @ lu[np.ix_(np.arange(c0, c1), rows)] if r else np.zeros((s, 0))
+        d_off.append(off)
+        vals.append(dblk.ravel())
+        off += s * s
+        m_off.append(off)
+        vals.append(mk.ravel())
+        off += r * s
+        n_off.append(off)
+        vals.append(nk.ravel())
+        off += s * r
+        col_ids.append(perm[c0:c1])
+        row_ids.append(perm[rows])
+    col_ptr = np.concatenate([[0], np.cumsum(sn_s)]).astype(np.int64)
+    row_ptr = np.concatenate([[0], np.cumsum(sn_r)]).astype(np.int64)
+    row_cat = np.concatenate(row_ids) if row_ids else np.zeros(0, dtype=np.int64)
+    # contributions to subtract from each column: every slot whose row id is
+    # that column, in ascending supernode (processing) order
+    slot_sn = np.repeat(np.arange(nsn), sn_r)
+    o = np.lexsort((slot_sn, row_cat))
+    g_idx = o.astype(np.int64)
+    g_ptr = np.concatenate([[0], np.cumsum(np.bincount(row_cat, minlength=n))]).astype(np.int64)
+    return CoarseFactor(n, level_ptr, sn_s, sn_r, col_ptr, np.concatenate(col_ids), row_ptr,
+                        row_cat, np.asarray(d_off, np.int64), np.asarray(m_off, np.int64),
+                        np.asarray(n_off, np.int64), np.concatenate(vals), g_ptr, g_idx)
+
+
+def solve_host(f: CoarseFactor, u: np.ndarray) -> np.ndarray:
+    """The device algorithm restated in numpy (level by level), for tests."""
+    y = np.zeros(f.n)
+    x = np.zeros(f.n)
+    cbuf = np.zeros(f.row_ptr[-1])
+    for lv in range(f.n_levels):
+        for k in range(f.level_ptr[lv], f.level_ptr[lv + 1]):
+            s, r = f.sn_s[k], f.sn_r[k]
+            cols = f.col_ids[f.col_ptr[k]:f.col_ptr[k + 1]]
+            bt = u[cols].astype(np.float64).copy()
+            for i, c in enumerate(cols):
+                for p in f.g_idx[f.g_ptr[c]:f.g_ptr[c + 1]]:
+                    bt[i] -= cbuf[p]
+            d = f.values[f.d_off[k]:f.d_off[k] + s * s].reshape(s, s)
+            linv = np.tril(d, -1) + np.eye(s)
+            y[cols] = linv @ bt
+            if r:
+                mk = f.values[f.m_off[k]:f.m_off[k] + r * s].reshape(r, s)
+                cbuf[f.row_ptr[k]:f.row_ptr[k + 1]] = mk @ bt
+    for lv in range(f.n_levels - 1, -1, -1):
+        for k in range(f.level_ptr[lv], f.level_ptr[lv + 1]):
+            s, r = f.sn_s[k], f.sn_r[k]
+            cols = f.col_ids[f.col_ptr[k]:f.col_ptr[k + 1]]
+            d = f.values[f.d_off[k]:f.d_off[k] + s * s].reshape(s, s)
+            xk = np.triu(d) @ y[cols]
+            if r:
+                nk = f.values[f.n_off[k]:f.n_off[k] + s * r].reshape(s, r)
+                xk = xk - nk @ x[f.row_ids[f.row_ptr[k]:f.row_ptr[k + 1]]]
+            x[cols] = xk
+    return x

@@ -35,6 +35,8 @@ CONFIGS = {
     "C5_64": ("laplace", 128, 4, SolverSpec("fast_ilu", 0, 3, 5), "natural", "double"),
     "C5_216": ("laplace", 128, 6, SolverSpec("fast_ilu", 0, 3, 5), "natural", "double"),
     "C5_256": ("laplace", 128, (8, 8, 4), SolverSpec("fast_ilu", 0, 3, 5), "natural", "double"),
+    # large coarse spaces on one GPU (n_c = 8 (P-1)^3 style growth): 2,744 and 12,600
+    "C5_2048": ("laplace", 128, (16, 16, 8), SolverSpec("fast_ilu", 0, 3, 5), "natural", "double"),
 }
 
 
@@ -67,13 +69,40 @@ def run(name):
     e1.record()
     torch.cuda.synchronize()
     xh = x.cpu().numpy()
+    # preconditioner apply alone (side-stream overlap on), then one profiled
+    # pass (overlap off: every event interval is one kernel's own) for the
+    # coarse phase's share of the apply
+    from paper_2304_04876_b200 import device
+    r = torch.from_numpy(np.random.default_rng(1).standard_normal(prob.a.nrows)).cuda()
+    for _ in range(3):
+        pre.apply(r)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(20):
+        pre.apply(r)
+    e1.record()
+    torch.cuda.synchronize()
+    apply_ms = e0.elapsed_time(e1) / 20
+    device.prof_reset()
+    device.prof_enable(True)
+    for _ in range(5):
+        pre.apply(r)
+    torch.cuda.synchronize()
+    device.prof_enable(False)
+    ph = device.prof_read()
+    coarse_keys = [k for k in ph if k.startswith(("restrict", "coarse"))]
+    coarse_ms = sum(ph[k]["ms"] for k in coarse_keys) / 5
+    apply_prof_ms = sum(v["ms"] for v in ph.values()) / 5
     out = dict(config=name, n=prob.a.nrows, subdomains=px * py * pz,
                n_coarse=pre.coarse.a0.nrows if pre.coarse else 0,
                setup_s=dict(inputs=t_in, symbolic=t_sym, numeric=t_num),
                iterations=rep.iterations, converged=rep.converged,
                solve_ms=e0.elapsed_time(e1), ms_per_iteration=e0.elapsed_time(e1) / max(rep.iterations, 1),
                true_rel_residual=float(np.linalg.norm(b - prob.a @ xh) / np.linalg.norm(b)),
-               fill_nnz=int(sum(s.fill_nnz for s in skel.local_symbolics)))
+               fill_nnz=int(sum(s.fill_nnz for s in skel.local_symbolics)),
+               apply_ms=apply_ms, apply_profiled_ms=apply_prof_ms, coarse_phase_ms=coarse_ms,
+               coarse_share=coarse_ms / apply_prof_ms if apply_prof_ms else None,
+               phases_ms={k: round(v["ms"] / 5, 4) for k, v in ph.items()})
     print(json.dumps(out), flush=True)
 
 
