@@ -167,6 +167,34 @@ int gdsw_precond_get_panels(const gdsw_precond* m, double* panels);
 int gdsw_precond_coarse_galerkin(gdsw_precond* m, const gdsw_csr* a, double* a0_dense, uint8_t* pattern);
 /* dense A0^-1 (n_c x n_c, row-major, float64; cast to the precond dtype) */
 int gdsw_precond_set_coarse_inverse(gdsw_precond* m, const double* a0inv);
+/* factored coarse solve (replaces the reference's sparse LU of A0 and its
+ * level-set solves, schwarz.py:267-272, 305, for large n_c): supernodal
+ * partitioned inverse of the nested-dissection LU, built on the host by
+ * paper_2304_04876_b200/coarse_factor.py. Supernodes in processing order
+ * (leaves first), grouped by tree level; all index arrays are ORIGINAL coarse
+ * columns; values float64 (cast to the precond dtype); updates are passed
+ * up the supernode tree by extend-add. Replaces a dense
+ * inverse set before (and vice versa). */
+typedef struct gdsw_coarse_factor {
+  int32_t n, n_sn, n_levels;
+  const int64_t* level_ptr;   /* [n_levels + 1] supernode ranges */
+  const int64_t* sn_s;        /* [n_sn] columns */
+  const int64_t* sn_r;        /* [n_sn] rows below the diagonal block */
+  const int64_t* col_ptr;     /* [n_sn + 1] */
+  const int64_t* col_ids;
+  const int64_t* row_ptr;     /* [n_sn + 1] == contribution-buffer offsets */
+  const int64_t* row_ids;
+  const int64_t* d_off;       /* s x s: strict lower = L_kk^-1, upper = U_kk^-1 */
+  const int64_t* m_off;       /* r x s: L_{R,k} L_kk^-1 */
+  const int64_t* n_off;       /* s x r: U_kk^-1 U_{k,R} */
+  const int64_t* in_ptr;      /* [col_ptr[n_sn] + 1] children's update slots a column subtracts */
+  const int64_t* in_idx;
+  const int64_t* out_ptr;     /* [row_ptr[n_sn] + 1] children's update slots an update row adds */
+  const int64_t* out_idx;
+  const double* values;
+  int64_t n_values;
+} gdsw_coarse_factor;
+int gdsw_precond_set_coarse_factor(gdsw_precond* m, const gdsw_coarse_factor* f);
 /* z = Phi A0^-1 Phi^T r + sum_i R_i^T A_i^-1 R_i r  (apply, schwarz.py:290-327) */
 int gdsw_precond_apply(gdsw_precond* m, const double* r, double* z, void* stream);
 /* per-block solves only: y[k] (dtype, concatenated block rows, permuted) =

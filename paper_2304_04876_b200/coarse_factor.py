@@ -13,10 +13,12 @@ B200 path uses a supernodal PARTITIONED INVERSE of the nested-dissection LU:
   single-child chains amalgamated when the explicit zeros stay bounded),
   each with its column set C_k (s_k columns) and the rows R_k below it.
 * Forward solve, one kernel per supernode-tree level (leaves first): with
-  bt_k = b[C_k] - (contributions of descendants), the level computes
+  bt_k = b[C_k] - (children's updates on C_k), the level computes
   [y_k; c_k] = [L_kk^-1; L_{R_k,k} L_kk^-1] bt_k -- one dense GEMV per
-  supernode (no sequential substitution inside it); c_k is written to a
-  contribution buffer that the ancestors owning R_k gather in a fixed order.
+  supernode (no sequential substitution inside it); c_k plus the children's
+  updates on R_k is the supernode's
+  update buffer; a parent subtracts its children's updates on its columns
+  and passes the rest up (multifrontal extend-add, children in a fixed order).
 * Backward solve, one kernel per level (root first):
   x_k = [U_kk^-1 | -U_kk^-1 U_{k,R_k}] [y_k; x[R_k]].
 
@@ -52,8 +54,10 @@ class CoarseFactor:
     m_off: np.ndarray          # [n_sn] offset of M_k = L_Rk L_kk^-1   (r x s, row-major)
     n_off: np.ndarray          # [n_sn] offset of N_k = U_kk^-1 U_kR   (s x r, row-major)
     values: np.ndarray         # float64
-    g_ptr: np.ndarray          # [n + 1] by original column: contribution slots to subtract
-    g_idx: np.ndarray          # contribution buffer positions, ascending supernode order
+    in_ptr: np.ndarray         # [col_ptr[-1] + 1] children's update slots each column subtracts
+    in_idx: np.ndarray
+    out_ptr: np.ndarray        # [row_ptr[-1] + 1] children's update slots each update row adds
+    out_idx: np.ndarray
 
     @property
     def n_levels(self) -> int:
@@ -100,11 +104,9 @@ def _supernodes(nz: np.ndarray, max_zero_frac: float):
     explicit zeros stay under `max_zero_frac`. Returns (starts, parent_of_sn)."""
     n = nz.shape[0]
     cc = nz.sum(axis=0)
-    parent = np.full(n, -1, dtype=np.int64)
-    for j in range(n):
-        r = np.flatnonzero(nz[j + 1:, j])
-        if r.size:
-            parent[j] = j + 1 + r[0]
+    nzt = np.ascontiguousarray(nz.T)   # row j = column j (strictly below the diagonal)
+    parent = np.where(nzt.any(axis=1), nzt.argmax(axis=1), -1).astype(np.int64)
+    del nzt
     nchild = np.bincount(parent[parent >= 0], minlength=n)
     starts = [0]
     for j in range(1, n):
@@ -170,20 +172,30 @@ def build_coarse_factor(a0, perm: np.ndarray | None = None,
     starts, _ = _supernodes(nz, max_zero_frac)
     nsn = starts.size - 1
     sn_of = np.repeat(np.arange(nsn), np.diff(starts))
-    # supernode tree and levels (height from the leaves)
-    sn_rows = []
+    # supernode tree: R_k = rows below supernode k; parent = supernode of the
+    # first row. Extend-add needs R_c within C_p + R_p for every child c of p
+    # (true of the elimination tree; enforced here so numerically vanished
+    # entries cannot break it: missing rows join R_p as explicit zeros)
+    sn_rows = [np.flatnonzero(nz[starts[k + 1]:, starts[k]:starts[k + 1]].any(axis=1)) + starts[k + 1]
+               for k in range(nsn)]
+    del nz
     sn_par = np.full(nsn, -1, dtype=np.int64)
-    for k in range(nsn):
-        c0, c1 = starts[k], starts[k + 1]
-        rows = np.flatnonzero(nz[c1:, c0:c1].any(axis=1)) + c1
-        sn_rows.append(rows)
-        if rows.size:
-            sn_par[k] = sn_of[rows[0]]
-    height = np.zeros(nsn, dtype=np.int64)
     for k in range(nsn):  # children precede parents (ND postorder)
+        rows = sn_rows[k]
+        if rows.size:
+            p = sn_of[rows[0]]
+            sn_par[k] = p
+            above = rows[rows >= starts[p + 1]]
+            extra = np.setdiff1d(above, sn_rows[p], assume_unique=True)
+            if extra.size:
+                sn_rows[p] = np.union1d(sn_rows[p], extra)
+    height = np.zeros(nsn, dtype=np.int64)
+    for k in range(nsn):
         if sn_par[k] >= 0:
             height[sn_par[k]] = max(height[sn_par[k]], height[k] + 1)
-    order = np.lexsort((np.arange(nsn), height))
+    order = np.lexsort((np.arange(nsn), height))   # processing order, leaves first
+    pos_of = np.empty(nsn, dtype=np.int64)
+    pos_of[order] = np.arange(nsn)
     level_ptr = np.searchsorted(height[order], np.arange(height.max() + 2)).astype(np.int64)
     import scipy.linalg as sl
     vals, d_off, m_off, n_off = [], [], [], []
@@ -217,37 +229,101 @@ def build_coarse_factor(a0, perm: np.ndarray | None = None,
         row_ids.append(perm[rows])
     col_ptr = np.concatenate([[0], np.cumsum(sn_s)]).astype(np.int64)
     row_ptr = np.concatenate([[0], np.cumsum(sn_r)]).astype(np.int64)
-    row_cat = np.concatenate(row_ids) if row_ids else np.zeros(0, dtype=np.int64)
-    # contributions to subtract from each column: every slot whose row id is
-    # that column, in ascending supernode (processing) order
-    slot_sn = np.repeat(np.arange(nsn), sn_r)
-    o = np.lexsort((slot_sn, row_cat))
-    g_idx = o.astype(np.int64)
-    g_ptr = np.concatenate([[0], np.cumsum(np.bincount(row_cat, minlength=n))]).astype(np.int64)
+    # extend-add lists: the update vector of supernode p (over R_p, at
+    # row_ptr[p] in the buffer) = M_p bt_p + its children's updates at R_p;
+    # bt_p = u[C_p] - its children's updates at C_p. Children in processing
+    # order, so every sum has a fixed order.
+    children = [[] for _ in range(nsn)]
+    for q, k in enumerate(order):
+        if sn_par[k] >= 0:
+            children[pos_of[sn_par[k]]].append(q)
+    in_lists = [[] for _ in range(col_ptr[-1])]
+    out_lists = [[] for _ in range(row_ptr[-1])]
+    for q, k in enumerate(order):
+        c0, c1 = starts[k], starts[k + 1]
+        rows_p = sn_rows[k]
+        for qc in children[q]:
+            rc = sn_rows[order[qc]]
+            slots = row_ptr[qc] + np.arange(rc.size)
+            in_c = rc < c1
+            for g, slot in zip(rc[in_c], slots[in_c]):
+                in_lists[col_ptr[q] + (g - c0)].append(slot)
+            if (~in_c).any():
+                where = np.searchsorted(rows_p, rc[~in_c])
+                if not np.array_equal(rows_p[np.minimum(where, rows_p.size - 1)], rc[~in_c]):
+                    raise AssertionError("supernode tree violates R_c within C_p + R_p")
+                for w, slot in zip(where, slots[~in_c]):
+                    out_lists[row_ptr[q] + w].append(slot)
+
+    def flat(lists):
+        ptr = np.concatenate([[0], np.cumsum([len(x) for x in lists])]).astype(np.int64)
+        idx = np.asarray([v for x in lists for v in x], dtype=np.int64)
+        return ptr, idx
+
+    in_ptr, in_idx = flat(in_lists)
+    out_ptr, out_idx = flat(out_lists)
     return CoarseFactor(n, level_ptr, sn_s, sn_r, col_ptr, np.concatenate(col_ids), row_ptr,
-                        row_cat, np.asarray(d_off, np.int64), np.asarray(m_off, np.int64),
-                        np.asarray(n_off, np.int64), np.concatenate(vals), g_ptr, g_idx)
+                        np.concatenate(row_ids) if row_ids else np.zeros(0, np.int64),
+                        np.asarray(d_off, np.int64), np.asarray(m_off, np.int64),
+                        np.asarray(n_off, np.int64), np.concatenate(vals),
+                        in_ptr, in_idx, out_ptr, out_idx)
+
+
+# n_c from which the factored solve replaces the dense inverse GEMV
+# (GDSW_COARSE_FACTOR=1 / =0 forces either)
+FACTOR_MIN_NC = 2000
+
+
+def dense_inverse(a0) -> np.ndarray:
+    """A0^-1 (float64) for the dense coarse GEMV; computed on the device
+    (cuSOLVER through torch) when one is present."""
+    dense = np.asarray(a0.to_dense(), dtype=np.float64)
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.linalg.inv(torch.from_numpy(dense).cuda()).cpu().numpy()
+    except ImportError:  # pragma: no cover
+        pass
+    return np.linalg.inv(dense)
+
+
+def install(pre, a0) -> str:
+    """Give the device preconditioner `pre` its coarse solve for A0:
+    the factored partitioned inverse for large n_c, else the dense inverse.
+    Returns the kind installed."""
+    import os
+    mode = os.environ.get("GDSW_COARSE_FACTOR", "auto")
+    if mode == "1" or (mode != "0" and a0.nrows >= FACTOR_MIN_NC):
+        pre.set_coarse_factor(build_coarse_factor(a0))
+        return "factor"
+    pre.set_coarse_inverse(dense_inverse(a0))
+    return "dense"
 
 
 def solve_host(f: CoarseFactor, u: np.ndarray) -> np.ndarray:
     """The device algorithm restated in numpy (level by level), for tests."""
     y = np.zeros(f.n)
     x = np.zeros(f.n)
-    cbuf = np.zeros(f.row_ptr[-1])
+    ubuf = np.zeros(f.row_ptr[-1])
     for lv in range(f.n_levels):
         for k in range(f.level_ptr[lv], f.level_ptr[lv + 1]):
             s, r = f.sn_s[k], f.sn_r[k]
             cols = f.col_ids[f.col_ptr[k]:f.col_ptr[k + 1]]
             bt = u[cols].astype(np.float64).copy()
-            for i, c in enumerate(cols):
-                for p in f.g_idx[f.g_ptr[c]:f.g_ptr[c + 1]]:
-                    bt[i] -= cbuf[p]
+            for i in range(s):
+                g = f.col_ptr[k] + i
+                for p in f.in_idx[f.in_ptr[g]:f.in_ptr[g + 1]]:
+                    bt[i] -= ubuf[p]
             d = f.values[f.d_off[k]:f.d_off[k] + s * s].reshape(s, s)
-            linv = np.tril(d, -1) + np.eye(s)
-            y[cols] = linv @ bt
+            y[cols] = (np.tril(d, -1) + np.eye(s)) @ bt
             if r:
                 mk = f.values[f.m_off[k]:f.m_off[k] + r * s].reshape(r, s)
-                cbuf[f.row_ptr[k]:f.row_ptr[k + 1]] = mk @ bt
+                upd = mk @ bt
+                for m in range(r):
+                    g = f.row_ptr[k] + m
+                    for p in f.out_idx[f.out_ptr[g]:f.out_ptr[g + 1]]:
+                        upd[m] += ubuf[p]
+                ubuf[f.row_ptr[k]:f.row_ptr[k + 1]] = upd
     for lv in range(f.n_levels - 1, -1, -1):
         for k in range(f.level_ptr[lv], f.level_ptr[lv + 1]):
             s, r = f.sn_s[k], f.sn_r[k]

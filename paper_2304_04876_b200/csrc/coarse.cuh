@@ -304,9 +304,19 @@ __global__ void k_coarse_gemv(int32_t n_c, const T* __restrict__ ainv, const T* 
   const int lane = threadIdx.x & 31;
   if (i >= n_c) return;
   const T* row = ainv + (int64_t)i * n_c;
-  T acc = T(0);
-  for (int32_t j = lane; j < n_c; j += 32) acc += ldg_stream(row + j) * u[j];
-  acc = warp_sum(acc);
+  // four independent partial sums: four row loads in flight per lane
+  T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+  int32_t j = lane;
+  for (; j + 96 < n_c; j += 128) {
+    const T r0 = ldg_stream(row + j), r1 = ldg_stream(row + j + 32), r2 = ldg_stream(row + j + 64),
+            r3 = ldg_stream(row + j + 96);
+    a0 += r0 * u[j];
+    a1 += r1 * u[j + 32];
+    a2 += r2 * u[j + 64];
+    a3 += r3 * u[j + 96];
+  }
+  for (; j < n_c; j += 32) a0 += ldg_stream(row + j) * u[j];
+  const T acc = warp_sum((a0 + a1) + (a2 + a3));
   if (lane == 0) v[i] = acc;
 }
 

@@ -12,6 +12,7 @@
 
 #include "../../include/gdsw.h"
 #include "coarse.cuh"
+#include "coarse_factor.cuh"
 #include "common.cuh"
 #include "dist.cuh"
 #include "extension.cuh"
@@ -580,6 +581,21 @@ struct gdsw_precond {
   DBuf<double> panel64;
   DBuf<char> panel32;              // f32 copy when dtype == F32
   DBuf<char> pgr_val, pgt_val, ainv;
+  // factored coarse solve (coarse_factor.cuh); used instead of ainv when set
+  struct CoarseFactorBuf {
+    bool on = false;
+    DBuf<int32_t> sn_s, sn_r, col_ptr, col_ids, row_ptr, row_ids, in_ptr, in_idx, out_ptr, out_idx;
+    DBuf<int64_t> d_off, m_off, n_off;
+    DBuf<int2> tasks;
+    std::vector<int32_t> fwd_ptr, bwd_ptr;  // per level: task ranges (forward, backward)
+    std::vector<size_t> fwd_smem, bwd_smem;
+    DBuf<char> vals, ybuf, cbuf;
+    int64_t bytes = 0;
+    CoarseFactorDev dev() const {
+      return CoarseFactorDev{sn_s.p, sn_r.p, col_ptr.p, col_ids.p, row_ptr.p, row_ids.p,
+                             d_off.p, m_off.p, n_off.p, in_ptr.p, in_idx.p, out_ptr.p, out_idx.p};
+    }
+  } cf;
   DBuf<char> xb, x1, x2, x3, pdot, cu, cv;
   // recursive: a GMRES solve holds it for its whole duration and its
   // eager passes re-enter precond_apply
@@ -745,16 +761,32 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   return cur;
 }
 
-template <typename T, typename CT, bool SMEMX, bool FWD = false>
-void launch_stream(gdsw_precond* m, const double* r, T* y, int32_t ring, size_t smem, cudaStream_t s) {
+template <typename T, typename CT, bool SMEMX, bool FWD, int NW>
+void launch_stream_nw(gdsw_precond* m, const double* r, T* y, int32_t ring, size_t smem, cudaStream_t s) {
   static bool attr = [] {
-    CK(cudaFuncSetAttribute(k_trisolve_stream<T, CT, SMEMX, FWD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(k_trisolve_stream<T, CT, SMEMX, FWD, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             FWD ? 200 * 1024 : 220 * 1024));
     return true;
   }();
   (void)attr;
-  k_trisolve_stream<T, CT, SMEMX, FWD><<<m->plan->n_sub, TR_THREADS_ALL, smem, s>>>(
+  k_trisolve_stream<T, CT, SMEMX, FWD, NW><<<m->plan->n_sub, 32 * NW + 32, smem, s>>>(
       m->tstream.view(), ring, m->plan->sub_ptr.p, m->plan->gmap.p, r, y);
+}
+
+// consumer warps per CTA: 8 when blocks outnumber the SMs (several CTAs
+// per SM), else 16 (fewer rows per warp on each level's critical path:
+// C2 ILU(0) local solve 0.377 -> 0.303 ms, C3-sized blocks 1.51 -> 1.43 ms);
+// GDSW_TS_WARPS=8/16/24 forces
+template <typename T, typename CT, bool SMEMX, bool FWD = false>
+void launch_stream(gdsw_precond* m, const double* r, T* y, int32_t ring, size_t smem, cudaStream_t s) {
+  static const int nw_env = [] {
+    const char* e = std::getenv("GDSW_TS_WARPS");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int nw = nw_env ? nw_env : (m->plan->n_sub > num_sms() ? 8 : 16);
+  if (nw == 24) launch_stream_nw<T, CT, SMEMX, FWD, 24>(m, r, y, ring, smem, s);
+  else if (nw == 16) launch_stream_nw<T, CT, SMEMX, FWD, 16>(m, r, y, ring, smem, s);
+  else launch_stream_nw<T, CT, SMEMX, FWD, 8>(m, r, y, ring, smem, s);
 }
 
 template <typename T>
@@ -838,6 +870,36 @@ T* local_solve(gdsw_precond* m, const double* r, int jacobi_iters, cudaStream_t 
   return levelset_solve<T>(m, r, s);
 }
 
+// v = A0^-1 u: dense inverse GEMV, or the factored partitioned inverse
+// (one launch per tree level and direction)
+template <typename T>
+void coarse_solve(gdsw_precond* m, cudaStream_t cs) {
+  CoarsePlan* Cp = m->cp.get();
+  if (!m->cf.on) {
+    ProfScope ps("coarse_solve", cs, (double)Cp->n_c * Cp->n_c * sizeof(T));
+    k_coarse_gemv<T><<<grid_for(Cp->n_c, TB / 32), TB, 0, cs>>>(Cp->n_c, (const T*)m->ainv.p,
+                                                                (const T*)m->cu.p, (T*)m->cv.p);
+    CK_LAUNCH();
+    return;
+  }
+  auto& F = m->cf;
+  ProfScope ps("coarse_solve", cs, (double)F.bytes);
+  const CoarseFactorDev D = F.dev();
+  const int nl = (int)F.fwd_smem.size();
+  for (int l = 0; l < nl; ++l) {
+    const int32_t t0 = F.fwd_ptr[l], nt = F.fwd_ptr[l + 1] - t0;
+    k_cf_forward<T><<<nt, CF_THREADS, F.fwd_smem[l], cs>>>(D, F.tasks.p + t0, (const T*)F.vals.p,
+                                                          (const T*)m->cu.p, (T*)F.ybuf.p, (T*)F.cbuf.p);
+    CK_LAUNCH();
+  }
+  for (int l = nl - 1; l >= 0; --l) {
+    const int32_t t0 = F.bwd_ptr[l], nt = F.bwd_ptr[l + 1] - t0;
+    k_cf_backward<T><<<nt, CF_THREADS, F.bwd_smem[l], cs>>>(D, F.tasks.p + t0, (const T*)F.vals.p,
+                                                           (const T*)F.ybuf.p, (T*)m->cv.p);
+    CK_LAUNCH();
+  }
+}
+
 template <typename T>
 void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
   gdsw_plan* P = m->plan;
@@ -884,10 +946,7 @@ void apply_T(gdsw_precond* m, const double* r, double* z, cudaStream_t s) {
       k_cast_from_f64<T><<<grid_for(Cp->n_c, TB), TB, 0, cs>>>(Cp->n_c, m->red64.p + Cp->n_c, (T*)m->cu.p);
       CK_LAUNCH();
     }
-    ProfScope ps("coarse_solve", cs, (double)Cp->n_c * Cp->n_c * sizeof(T));
-    k_coarse_gemv<T><<<grid_for(Cp->n_c, TB / 32), TB, 0, cs>>>(Cp->n_c, (const T*)m->ainv.p,
-                                                                (const T*)m->cu.p, (T*)m->cv.p);
-    CK_LAUNCH();
+    coarse_solve<T>(m, cs);
   }
   if (fork) CK(cudaEventRecord(m->ev_join, m->side));
   T* y = local_solve<T>(m, r, 0, s);
@@ -1427,6 +1486,79 @@ int gdsw_precond_set_coarse_inverse(gdsw_precond* m, const double* a0inv) {
     CoarsePlan* P = m->cp.get();
     std::vector<double> h(a0inv, a0inv + (size_t)P->n_c * P->n_c);
     with_dtype(m->dtype, [&](auto tag) { upload_cast<decltype(tag)>(m->ainv, h); });
+    m->cf.on = false;
+    m->has_ainv = true;
+    m->drop_graphs();
+  });
+}
+
+int gdsw_precond_set_coarse_factor(gdsw_precond* m, const gdsw_coarse_factor* f) {
+  return guarded([&] {
+    require(m->cp != nullptr, "preconditioner has no coarse structure");
+    require(f->n == m->cp->n_c, "coarse factor dimension mismatch");
+    auto& F = m->cf;
+    const int nsn = f->n_sn, nl = f->n_levels;
+    auto i32 = [](const int64_t* a, size_t n) { return to_i32(a, n); };
+    F.sn_s.upload(i32(f->sn_s, nsn));
+    F.sn_r.upload(i32(f->sn_r, nsn));
+    F.col_ptr.upload(i32(f->col_ptr, nsn + 1));
+    F.row_ptr.upload(i32(f->row_ptr, nsn + 1));
+    F.col_ids.upload(i32(f->col_ids, f->col_ptr[nsn]));
+    F.row_ids.upload(i32(f->row_ids, f->row_ptr[nsn]));
+    const int64_t ncol = f->col_ptr[nsn], nrow = f->row_ptr[nsn];
+    F.in_ptr.upload(i32(f->in_ptr, ncol + 1));
+    F.in_idx.upload(i32(f->in_idx, f->in_ptr[ncol]));
+    F.out_ptr.upload(i32(f->out_ptr, nrow + 1));
+    F.out_idx.upload(i32(f->out_idx, f->out_ptr[nrow]));
+    F.d_off.upload(f->d_off, nsn);
+    F.m_off.upload(f->m_off, nsn);
+    F.n_off.upload(f->n_off, nsn);
+    // tasks: forward levels (CF_ROWS-row tiles of the stacked s + r rows),
+    // then backward levels (tiles of the s rows)
+    std::vector<int2> tasks;
+    F.fwd_ptr.assign(1, 0);
+    F.bwd_ptr.clear();
+    F.fwd_smem.assign(nl, 0);
+    F.bwd_smem.assign(nl, 0);
+    int64_t bytes = 0;
+    const size_t es = m->es;
+    for (int l = 0; l < nl; ++l) {
+      for (int64_t k = f->level_ptr[l]; k < f->level_ptr[l + 1]; ++k) {
+        const int64_t s = f->sn_s[k], r = f->sn_r[k];
+        for (int64_t q = 0; q < s + r; q += CF_ROWS) tasks.push_back(make_int2((int)k, (int)q));
+        F.fwd_smem[l] = std::max(F.fwd_smem[l], (size_t)s * es);
+        bytes += (s * (s - 1) / 2 + r * s) * (int64_t)es;
+      }
+      F.fwd_ptr.push_back((int32_t)tasks.size());
+    }
+    F.bwd_ptr.assign(1, (int32_t)tasks.size());
+    for (int l = 0; l < nl; ++l) {
+      for (int64_t k = f->level_ptr[l]; k < f->level_ptr[l + 1]; ++k) {
+        const int64_t s = f->sn_s[k], r = f->sn_r[k];
+        for (int64_t q = 0; q < s; q += CF_ROWS) tasks.push_back(make_int2((int)k, (int)q));
+        F.bwd_smem[l] = std::max(F.bwd_smem[l], (size_t)(s + r) * es);
+        bytes += (s * (s + 1) / 2 + r * s) * (int64_t)es;
+      }
+      F.bwd_ptr.push_back((int32_t)tasks.size());
+    }
+    size_t smax = 0;
+    for (int l = 0; l < nl; ++l) smax = std::max({smax, F.fwd_smem[l], F.bwd_smem[l]});
+    require(smax <= 200 * 1024, "coarse factor supernode too large for shared memory");
+    F.tasks.upload(tasks);
+    F.bytes = bytes;
+    with_dtype(m->dtype, [&](auto tag) {
+      using T = decltype(tag);
+      std::vector<double> h(f->values, f->values + f->n_values);
+      upload_cast<T>(F.vals, h);
+      F.ybuf.alloc((size_t)f->n * sizeof(T));
+      F.cbuf.alloc((size_t)std::max<int64_t>(f->row_ptr[nsn], 1) * sizeof(T));
+      if (smax > 48 * 1024) {
+        CK(cudaFuncSetAttribute(k_cf_forward<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+        CK(cudaFuncSetAttribute(k_cf_backward<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+      }
+    });
+    F.on = true;
+    m->ainv.release();
     m->has_ainv = true;
     m->drop_graphs();
   });

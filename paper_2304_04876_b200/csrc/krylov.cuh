@@ -51,7 +51,7 @@ __device__ __forceinline__ void sr_coef_compute(int j, const double* blk, double
 // all NR row loads of a step are independent (deep memory-level
 // parallelism). One shuffle tree per sum at the end, per-CTA partials in
 // fixed slots, the last CTA reduces them in CTA order (deterministic).
-template <int NR>
+template <int NR, int EP = 1>
 __global__ void __launch_bounds__(KDOT_THREADS, NR > 8 ? 1 : 2) k_block_dot(
     int64_t n, const double* __restrict__ V, int64_t ldv, int nv, int r0, int nrc,
     const double* __restrict__ v, const double* __restrict__ z, double* __restrict__ partial,
@@ -74,8 +74,43 @@ __global__ void __launch_bounds__(KDOT_THREADS, NR > 8 ? 1 : 2) k_block_dot(
   if (vec) {
     const int64_t n2 = n >> 1;
     const int32_t ld2 = (int32_t)(ldv >> 1);
+    int64_t i0 = tid;
+    if (EP == 2) {
+      // two element pairs per step: twice the independent loads in flight
+      // for the short blocks (few rows per thread)
 #pragma unroll 1
-    for (int64_t i = tid; i < n2; i += nth) {
+      for (; i0 + nth < n2; i0 += 2 * nth) {
+        double2 pv[2], pz[2], x[2][NR];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t ie = i0 + e * nth;
+          pv[e] = __ldg(reinterpret_cast<const double2*>(v) + ie);
+          pz[e] = z ? __ldg(reinterpret_cast<const double2*>(z) + ie) : make_double2(0.0, 0.0);
+          const double2* pb = reinterpret_cast<const double2*>(Vr) + ie;
+#pragma unroll
+          for (int u = 0; u < NR; ++u) {
+            if (u < nb) x[e][u] = ldg_stream(pb);
+            pb += ld2;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+#pragma unroll
+          for (int u = 0; u < NR; ++u) {
+            if (u < nb) {
+              av[u] = fma(x[e][u].y, pv[e].y, fma(x[e][u].x, pv[e].x, av[u]));
+              az[u] = fma(x[e][u].y, pz[e].y, fma(x[e][u].x, pz[e].x, az[u]));
+            }
+          }
+          if (self) {
+            as = fma(pv[e].y, pv[e].y, fma(pv[e].x, pv[e].x, as));
+            zs = fma(pv[e].y, pz[e].y, fma(pv[e].x, pz[e].x, zs));
+          }
+        }
+      }
+    }
+#pragma unroll 1
+    for (int64_t i = i0; i < n2; i += nth) {
       const double2 pv = __ldg(reinterpret_cast<const double2*>(v) + i);
       const double2 pz = z ? __ldg(reinterpret_cast<const double2*>(z) + i) : make_double2(0.0, 0.0);
       const double2* pb = reinterpret_cast<const double2*>(Vr) + i;
@@ -188,12 +223,14 @@ __global__ void __launch_bounds__(KDOT_THREADS, NR > 8 ? 1 : 2) k_block_dot(
 inline void launch_block_dot(unsigned grid, cudaStream_t s, int64_t n, const double* V, int64_t ldv,
                              int nv, int r0, int nrc, const double* v, const double* z,
                              double* partial, double* out, unsigned* counter, double* coef = nullptr) {
+  // EP = 2 (two element pairs per step) measured 5-20% faster for the 4- and
+  // 16-row buckets and neutral / slower for 8 (tools/micro/bench_blockdot2.cu)
   if (nrc <= 4)
-    k_block_dot<4><<<grid, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out, counter, coef);
+    k_block_dot<4, 2><<<grid, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out, counter, coef);
   else if (nrc <= 8)
     k_block_dot<8><<<grid, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out, counter, coef);
   else if (nrc <= 16)  // 32+ running sums: one CTA per SM (launch bound), half the grid
-    k_block_dot<16><<<(grid + 1) / 2, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out,
+    k_block_dot<16, 2><<<(grid + 1) / 2, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out,
                                                           counter, coef);
   else if (nrc <= 24)
     k_block_dot<24><<<(grid + 1) / 2, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out,

@@ -33,9 +33,8 @@
 
 namespace gdsw {
 
-constexpr int TR_CWARPS = 8;                    // consumer warps
-constexpr int TR_CTHREADS = 32 * TR_CWARPS;
-constexpr int TR_THREADS_ALL = TR_CTHREADS + 32;  // + producer warp
+// consumer warps per CTA: a template parameter NW (8, 16 or 32) of the
+// kernel, plus one TMA producer warp
 constexpr int TR_SHORT = 32;
 // previous-chunk forwarding: short-row results of a chunk are also kept in
 // shared memory (slot = position in the chunk), and the next chunk reads
@@ -575,8 +574,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+template <int NW>
 __device__ __forceinline__ void consumer_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(TR_CTHREADS) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * NW) : "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -584,7 +584,7 @@ __device__ __forceinline__ void consumer_bar() {
 // ---------------------------------------------------------------------------
 // supernode chunks (dense blocks of exact-LU separators). Rows are indexed
 // in solve order q: row(q) = brow + dir * q.
-template <typename T, typename CT>
+template <typename T, typename CT, int NW>
 __device__ __forceinline__ void ts_sn_chunk(const unsigned char* __restrict__ c, int type, bool up, T* x) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int4 h1 = *reinterpret_cast<const int4*>(c + 16);
@@ -595,7 +595,7 @@ __device__ __forceinline__ void ts_sn_chunk(const unsigned char* __restrict__ c,
     const int32_t q0 = h1.z, nq = h1.w, m = h2.x;
     const CT* E = reinterpret_cast<const CT*>(c + h2.y);
     const T* V = reinterpret_cast<const T*>(c + h2.z);
-    for (int t = warp; t < nq; t += TR_CWARPS) {
+    for (int t = warp; t < nq; t += NW) {
       const T* v = V + (int64_t)t * m;
       T acc = T(0);
 #pragma unroll 4
@@ -625,7 +625,7 @@ __device__ __forceinline__ void ts_sn_chunk(const unsigned char* __restrict__ c,
     // x[row_q] -= P_q . x[block jb], thread per row, panel column-major
     const int32_t jb = h1.z, nb = h1.w, q0 = h2.x, nq = h2.y;
     const T* P = reinterpret_cast<const T*>(c + h2.z);
-    for (int t = threadIdx.x; t < nq; t += TR_CTHREADS) {
+    for (int t = threadIdx.x; t < nq; t += (32 * NW)) {
       T acc = T(0);
       for (int j = 0; j < nb; ++j) acc = fma(P[(int64_t)j * nq + t], x[brow + dir * (jb + j)], acc);
       const int32_t row = brow + dir * (q0 + t);
@@ -634,20 +634,20 @@ __device__ __forceinline__ void ts_sn_chunk(const unsigned char* __restrict__ c,
   }
 }
 
-template <typename T, typename CT, bool FWD>
+template <typename T, typename CT, bool FWD, int NW>
 __device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T* x, T* part, const T* fprev,
                                          T* fcur) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int4 hdr = *reinterpret_cast<const int4*>(c);
   if (hdr.w != TR_ROWS) {
-    ts_sn_chunk<T, CT>(c, hdr.w, hdr.z & 1, x);
+    ts_sn_chunk<T, CT, NW>(c, hdr.w, hdr.z & 1, x);
     return;
   }
   const int nw = hdr.x, nsl = hdr.y;
   const bool up = hdr.z & 1, ordered = hdr.z & 2;
   const ChunkLayout cl(nw, nsl, up, (int)sizeof(T));
   // warp tasks (medium rows and segments of long rows)
-  for (int t = warp; t < nw; t += TR_CWARPS) {
+  for (int t = warp; t < nw; t += NW) {
     const int4 w = *reinterpret_cast<const int4*>(c + cl.wtab + 16 * t);
     const int2 gp = *reinterpret_cast<const int2*>(c + cl.wgrp + 8 * t);
     const int32_t row = w.x, len = w.y;
@@ -695,7 +695,7 @@ __device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T*
   // short rows: one thread each, sequential in column order
   const int32_t* srow = reinterpret_cast<const int32_t*>(c + cl.srow);
   const int32_t* slen = reinterpret_cast<const int32_t*>(c + cl.slen);
-  for (int t = threadIdx.x; t < 32 * nsl; t += TR_CTHREADS) {
+  for (int t = threadIdx.x; t < 32 * nsl; t += (32 * NW)) {
     const int32_t len = slen[t];
     if (len < 0) continue;
     const int32_t row = srow[t];
@@ -729,8 +729,8 @@ __device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T*
   if (hdr.z & 4) {
     // rows split in segments: partials summed in segment order by the
     // thread of the first segment once every segment is in
-    consumer_bar();
-    for (int t = threadIdx.x; t < nw; t += TR_CTHREADS) {
+    consumer_bar<NW>();
+    for (int t = threadIdx.x; t < nw; t += (32 * NW)) {
       const int2 gp = *reinterpret_cast<const int2*>(c + cl.wgrp + 8 * t);
       if (gp.y < 2 || gp.x != t) continue;
       const int32_t row = reinterpret_cast<const int4*>(c + cl.wtab)[t].x;
@@ -748,8 +748,8 @@ __device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T*
 // TR_NT in flight; a chunk never wraps), block solution written to y
 constexpr int TR_NT = 16;
 
-template <typename T, typename CT, bool SMEMX, bool FWD>
-__global__ void __launch_bounds__(TR_THREADS_ALL) k_trisolve_stream(TriStreamDev S, int32_t ring_bytes,
+template <typename T, typename CT, bool SMEMX, bool FWD, int NW>
+__global__ void __launch_bounds__(32 * NW + 32) k_trisolve_stream(TriStreamDev S, int32_t ring_bytes,
                                                                     const int32_t* __restrict__ sub_ptr,
                                                                     const int32_t* __restrict__ gmap,
                                                                     const double* __restrict__ r,
@@ -773,7 +773,7 @@ __global__ void __launch_bounds__(TR_THREADS_ALL) k_trisolve_stream(TriStreamDev
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (threadIdx.x >= TR_CTHREADS) {
+  if (threadIdx.x >= (32 * NW)) {
     // producer warp: the chunk table is read 32 entries at a time, one
     // window ahead; lane 0 issues the copies
     const int lane = threadIdx.x & 31;
@@ -816,18 +816,18 @@ __global__ void __launch_bounds__(TR_THREADS_ALL) k_trisolve_stream(TriStreamDev
     }
     return;
   }
-  for (int32_t k = threadIdx.x; k < ns; k += TR_CTHREADS) x[k] = (T)r[gmap[base + k]];
-  consumer_bar();
+  for (int32_t k = threadIdx.x; k < ns; k += (32 * NW)) x[k] = (T)r[gmap[base + k]];
+  consumer_bar<NW>();
   for (int i = 0; i < nch; ++i) {
     const int t = i % TR_NT;
     mbar_wait(&full[t], (uint32_t)((i / TR_NT) & 1));
-    ts_chunk<T, CT, FWD>(ring + pos[t], x, part, fwdbuf + ((i & 1) ^ 1) * (FWD ? TR_FWD : 0),
+    ts_chunk<T, CT, FWD, NW>(ring + pos[t], x, part, fwdbuf + ((i & 1) ^ 1) * (FWD ? TR_FWD : 0),
                          fwdbuf + (i & 1) * (FWD ? TR_FWD : 0));
-    consumer_bar();
+    consumer_bar<NW>();
     if (threadIdx.x == 0) mbar_arrive(&empty[t]);
   }
   if (SMEMX)
-    for (int32_t k = threadIdx.x; k < ns; k += TR_CTHREADS) y[base + k] = x[k];
+    for (int32_t k = threadIdx.x; k < ns; k += (32 * NW)) y[base + k] = x[k];
 }
 
 }  // namespace gdsw

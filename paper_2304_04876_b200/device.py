@@ -37,6 +37,16 @@ class _CoarseDesc(C.Structure):
             "col_ids", "aii_ptr", "aii_col", "aii_src", "aig_ptr", "aig_col", "aig_src")]
 
 
+_CF_ARRAYS = ("level_ptr", "sn_s", "sn_r", "col_ptr", "col_ids", "row_ptr", "row_ids", "d_off",
+              "m_off", "n_off", "in_ptr", "in_idx", "out_ptr", "out_idx")
+
+
+class _CoarseFactor(C.Structure):
+    _fields_ = ([("n", C.c_int32), ("n_sn", C.c_int32), ("n_levels", C.c_int32)] +
+                [(k, C.c_void_p) for k in _CF_ARRAYS] +
+                [("values", C.c_void_p), ("n_values", C.c_int64)])
+
+
 class _KrylovCfg(C.Structure):
     _fields_ = [("restart", C.c_int32), ("rel_tol", C.c_double), ("max_iters", C.c_int32),
                 ("variant", C.c_int32), ("orthogonalization", C.c_int32)]
@@ -76,6 +86,7 @@ _SIGS = {
     "gdsw_precond_panel_entries": (C.c_int64, [C.c_void_p]),
     "gdsw_precond_get_panels": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gdsw_precond_set_coarse_inverse": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gdsw_precond_set_coarse_factor": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gdsw_precond_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "gdsw_precond_local_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                            C.c_void_p]),
@@ -368,6 +379,14 @@ class Precond:
     def set_coarse_inverse(self, a0inv: np.ndarray):
         a = np.ascontiguousarray(a0inv, dtype=np.float64)
         _ck(_lib.gdsw_precond_set_coarse_inverse(self.handle, _ptr(a)))
+
+    def set_coarse_factor(self, f):
+        """Factored coarse solve (coarse_factor.CoarseFactor)."""
+        keep = {k: np.ascontiguousarray(getattr(f, k), dtype=np.int64) for k in _CF_ARRAYS}
+        vals = np.ascontiguousarray(f.values, dtype=np.float64)
+        d = _CoarseFactor(n=f.n, n_sn=f.n_sn, n_levels=f.n_levels, values=vals.ctypes.data,
+                          n_values=vals.size, **{k: v.ctypes.data for k, v in keep.items()})
+        _ck(_lib.gdsw_precond_set_coarse_factor(self.handle, C.byref(d)))
 
     def apply(self, r, z):
         _ck(_lib.gdsw_precond_apply(self.handle, _ptr(r), _ptr(z), stream_handle()))

@@ -247,7 +247,8 @@ class DistPreconditioner:
             self.a0_factorization = numeric_lu(a0, symbolic_lu(a0, make_ordering(a0, config.ordering)))
         except np.linalg.LinAlgError as err:
             raise np.linalg.LinAlgError(f"coarse matrix is singular: {err}") from err
-        self.pre.set_coarse_inverse(np.linalg.inv(a0.to_dense().astype(np.float64)))
+        from .coarse_factor import install as _install_coarse
+        _install_coarse(self.pre, a0)
         self.a0 = a0
         self.phi_local = phi_ext
         self.column_map = column_map

@@ -415,6 +415,7 @@ def setup_numeric(skeleton: PreconditionerSkeleton, a: CsrMatrix,
             pass
 
     n_sub = len(skeleton.sets)
+    tick = _setup_clock()
     if spec.method == "fast_ilu":
         if spec.factor_sweeps < 1:
             raise ValueError("factor_sweeps must be at least 1")
@@ -474,6 +475,7 @@ def setup_numeric(skeleton: PreconditionerSkeleton, a: CsrMatrix,
                                            trisolve_iters=spec.trisolve_iters))
         pre.set_factors(_cat(lvs, value_dtype), _cat(uvs, value_dtype))
 
+    tick("local factors")
     coarse = None
     if config.use_coarse:
         if nullspace is None:
@@ -484,7 +486,9 @@ def setup_numeric(skeleton: PreconditionerSkeleton, a: CsrMatrix,
                                                 skeleton.interior_sets, lazy_phi=True)
         # A0 = Phi^T A Phi on the GPU from the float64 panels, with the
         # reference's SpGEMM pattern (coarse_matrix, coarse_space.py:205-207)
+        tick("harmonic extension")
         a0 = pre.coarse_galerkin(a_src_dev, len(column_map))
+        tick("galerkin A0")
         phi = phi64
         if single:
             phi = lambda: convert_precision(phi64(), np.float32)  # noqa: E731
@@ -493,7 +497,10 @@ def setup_numeric(skeleton: PreconditionerSkeleton, a: CsrMatrix,
             a0_fac = numeric_lu(a0, symbolic_lu(a0, make_ordering(a0, config.ordering)))
         except np.linalg.LinAlgError as err:
             raise np.linalg.LinAlgError(f"coarse matrix is singular: {err}") from err
-        pre.set_coarse_inverse(np.linalg.inv(a0.to_dense().astype(np.float64)))
+        tick("A0 sparse LU (pivot check)")
+        from .coarse_factor import install as _install_coarse
+        kind = _install_coarse(pre, a0)
+        tick(f"coarse solve ({kind})")
         coarse = CoarseSolver(phi, None, a0, a0_fac, column_map)
 
     m = TwoLevelPreconditioner(skeleton.n, skeleton.sets, facs, coarse, config.precision,
@@ -502,6 +509,22 @@ def setup_numeric(skeleton: PreconditionerSkeleton, a: CsrMatrix,
         if f._l_values is None:
             f._source = (m, s)
     return m
+
+
+def _setup_clock():
+    """GDSW_SETUP_TIMES=1: print the numeric setup's phase times to stderr."""
+    import os
+    import sys
+    import time
+    if os.environ.get("GDSW_SETUP_TIMES") != "1":
+        return lambda label: None
+    t = [time.perf_counter()]
+
+    def tick(label):
+        now = time.perf_counter()
+        print(f"[setup_numeric] {label}: {now - t[0]:.3f} s", file=sys.stderr, flush=True)
+        t[0] = now
+    return tick
 
 
 def _gpu_lu_pays(spec, symbolics) -> bool:
