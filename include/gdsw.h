@@ -195,6 +195,12 @@ typedef struct gdsw_coarse_factor {
   int64_t n_values;
 } gdsw_coarse_factor;
 int gdsw_precond_set_coarse_factor(gdsw_precond* m, const gdsw_coarse_factor* f);
+/* exact-LU local solves through supernodal partitioned inverses of every
+ * block's factors in one batch (LocalFactorization.solve, local_solvers.py:
+ * 263-278, replacing the level-set substitution, _kernels.py:473-496);
+ * indices are positions in the concatenated block vector (block order, ND
+ * permutation folded in). NULL removes it (level-set path again). */
+int gdsw_precond_set_local_factor(gdsw_precond* m, const gdsw_coarse_factor* f);
 /* z = Phi A0^-1 Phi^T r + sum_i R_i^T A_i^-1 R_i r  (apply, schwarz.py:290-327) */
 int gdsw_precond_apply(gdsw_precond* m, const double* r, double* z, void* stream);
 /* per-block solves only: y[k] (dtype, concatenated block rows, permuted) =

@@ -104,6 +104,20 @@ int gh_classify_interface(int64_t n_nodes, const int64_t* g_ptr,
                           const int64_t* g_idx, const int64_t* node_owner,
                           gh_result** out);
 /* {iface_nodes, mult, piece_ptr, piece_nodes, key_ptr, keys, kind} */
+/* supernodal partitioned inverses of nblk exact-LU factors in one batch
+ * (the device solve of coarse_factor.cuh): block b has blk_n[b] rows, its
+ * CSR L (strictly lower, unit diagonal implied) at lp + lp_off[b] /
+ * li, lv + lnz_off[b] and U (diagonal first) at up + up_off[b] / ui, uv +
+ * unz_off[b], in its own ND-permuted numbering; blk_base[b] = its offset in
+ * the concatenated block vector. Result: {level_ptr, sn_s, sn_r, col_ptr,
+ * col_ids, row_ptr, row_ids, d_off, m_off, n_off, values (f64), in_ptr,
+ * in_idx, out_ptr, out_idx} -- include/gdsw.h gdsw_coarse_factor. */
+int gh_partitioned_inverse(int64_t nblk, const int64_t* blk_n, const int64_t* blk_base,
+                           const int64_t* lp_off, const int64_t* lnz_off, const int64_t* up_off,
+                           const int64_t* unz_off, const int64_t* lp, const int64_t* li,
+                           const double* lv, const int64_t* up, const int64_t* ui,
+                           const double* uv, int64_t relax, double zero_frac, int64_t threads,
+                           gh_result** out);
 
 #ifdef __cplusplus
 }

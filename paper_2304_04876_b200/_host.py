@@ -190,3 +190,23 @@ def overlap_sets(g_ptr, g_idx, node_owner, n_parts: int, subs, layers: int):
                        _p(node_owner), C.c_int64(n_parts), C.c_int64(subs.size), _p(subs),
                        C.c_int64(layers))
     return [nodes[ptr[k]:ptr[k + 1]] for k in range(subs.size)]
+
+
+def partitioned_inverse(blocks, relax: int, zero_frac: float, threads: int):
+    """Supernodal partitioned inverses of exact-LU blocks (gh_partitioned_inverse).
+    blocks = [(base, l_ptr, l_idx, l_val, u_ptr, u_idx, u_val)]; returns the
+    15 arrays of coarse_factor.CoarseFactor in ABI order."""
+    nb = len(blocks)
+    blk_n = _i64([b[1].size - 1 for b in blocks])
+    base = _i64([b[0] for b in blocks])
+    lp_off = _i64(np.concatenate([[0], np.cumsum([b[1].size for b in blocks])])[:-1])
+    up_off = _i64(np.concatenate([[0], np.cumsum([b[4].size for b in blocks])])[:-1])
+    lnz_off = _i64(np.concatenate([[0], np.cumsum([b[2].size for b in blocks])])[:-1])
+    unz_off = _i64(np.concatenate([[0], np.cumsum([b[5].size for b in blocks])])[:-1])
+    cat = (lambda k, dt: np.ascontiguousarray(np.concatenate([b[k] for b in blocks]), dtype=dt)
+           if blocks else np.zeros(0, dtype=dt))
+    lp, li, lv = cat(1, np.int64), cat(2, np.int64), cat(3, np.float64)
+    up, ui, uv = cat(4, np.int64), cat(5, np.int64), cat(6, np.float64)
+    return _call(_lib.gh_partitioned_inverse, C.c_int64(nb), _p(blk_n), _p(base), _p(lp_off),
+                 _p(lnz_off), _p(up_off), _p(unz_off), _p(lp), _p(li), _p(lv), _p(up), _p(ui),
+                 _p(uv), C.c_int64(relax), C.c_double(zero_frac), C.c_int64(threads))

@@ -151,6 +151,146 @@ def _supernodes(nz: np.ndarray, max_zero_frac: float):
     return starts, parent
 
 
+# supernodes smaller than this merge into their parent (relaxed amalgamation)
+RELAX = 32
+
+
+def _records_from_lu(lu: np.ndarray, keys: np.ndarray, ids: np.ndarray, max_zero_frac: float):
+    """Supernode records of one factor (dense combined L\\U `lu` of the
+    permuted matrix). keys[j] = a globally unique, increasing key of ND
+    position j (matching), ids[j] = the vector index it solves for."""
+    import scipy.linalg as sl
+    if not np.all(np.isfinite(lu)) or np.any(np.diag(lu) == 0.0):
+        raise np.linalg.LinAlgError("matrix is singular")
+    n = lu.shape[0]
+    nz = (np.tril(lu, -1) != 0.0) | (np.triu(lu, 1).T != 0.0)
+    starts, _ = _supernodes(nz, max_zero_frac)
+    nsn = starts.size - 1
+    sn_of = np.repeat(np.arange(nsn), np.diff(starts))
+    # R_k = rows below supernode k; parent = supernode of the first row.
+    # Extend-add needs R_c within C_p + R_p for every child c of p (true of
+    # the elimination tree; enforced here so numerically vanished entries
+    # cannot break it: missing rows join R_p as explicit zeros)
+    rows_of = [np.flatnonzero(nz[starts[k + 1]:, starts[k]:starts[k + 1]].any(axis=1)) + starts[k + 1]
+               for k in range(nsn)]
+    del nz
+    cols_of = [np.arange(starts[k], starts[k + 1]) for k in range(nsn)]
+    par = np.full(nsn, -1, dtype=np.int64)
+    for k in range(nsn):  # children precede parents (ND postorder)
+        rows = rows_of[k]
+        if rows.size:
+            p = sn_of[rows[0]]
+            par[k] = p
+            above = rows[rows >= starts[p + 1]]
+            extra = np.setdiff1d(above, rows_of[p], assume_unique=True)
+            if extra.size:
+                rows_of[p] = np.union1d(rows_of[p], extra)
+    # relaxed amalgamation: a small supernode joins its parent (any child,
+    # not only a single one) while the merged column set stays <= RELAX:
+    # cuts the tree height (launches) that chains of tiny leaves cost
+    rep = np.arange(nsn)
+
+    def find(k):
+        while rep[k] != k:
+            rep[k] = rep[rep[k]]
+            k = rep[k]
+        return k
+
+    for k in range(nsn):
+        if par[k] < 0:
+            continue
+        p = find(par[k])
+        if cols_of[k].size + cols_of[p].size <= RELAX:
+            cols_of[p] = np.union1d(cols_of[p], cols_of[k])
+            rows_of[p] = np.setdiff1d(np.union1d(rows_of[p], rows_of[k]), cols_of[p])
+            rep[k] = p
+            cols_of[k] = rows_of[k] = None
+    alive = [k for k in range(nsn) if rep[k] == k]
+    newid = {k: q for q, k in enumerate(alive)}
+    par2 = np.full(len(alive), -1, dtype=np.int64)
+    for q, k in enumerate(alive):
+        if rows_of[k].size:
+            par2[q] = newid[find(sn_of[rows_of[k][0]])]
+    height = np.zeros(len(alive), dtype=np.int64)
+    for q in range(len(alive)):  # parents after children (ascending first column)
+        if par2[q] >= 0:
+            height[par2[q]] = max(height[par2[q]], height[q] + 1)
+    recs = []
+    for q, k in enumerate(alive):
+        cols, rows = cols_of[k], rows_of[k]
+        s = cols.size
+        blk = lu[np.ix_(cols, cols)]
+        linv = sl.solve_triangular(np.tril(blk, -1) + np.eye(s), np.eye(s), lower=True,
+                                   unit_diagonal=True)
+        uinv = sl.solve_triangular(np.triu(blk), np.eye(s), lower=False)
+        recs.append(dict(
+            level=int(height[q]), parent=int(par2[q]),
+            col_keys=keys[cols], row_keys=keys[rows], cols=ids[cols], rows=ids[rows],
+            d=np.tril(linv, -1) + np.triu(uinv),
+            m=lu[np.ix_(rows, cols)] @ linv,
+            nmat=uinv @ lu[np.ix_(cols, rows)]))
+    return recs
+
+
+def _assemble(recs: list, n: int) -> CoarseFactor:
+    """Sort supernode records by tree level (leaves first; stable across
+    blocks) and emit the device arrays with the extend-add lists."""
+    order = sorted(range(len(recs)), key=lambda q: (recs[q]["level"], q))
+    pos = np.empty(len(recs), dtype=np.int64)
+    pos[order] = np.arange(len(recs))
+    levels = np.asarray([recs[q]["level"] for q in order], dtype=np.int64)
+    level_ptr = np.searchsorted(levels, np.arange(levels.max(initial=0) + 2)).astype(np.int64)
+    sn_s = np.asarray([recs[q]["cols"].size for q in order], dtype=np.int64)
+    sn_r = np.asarray([recs[q]["rows"].size for q in order], dtype=np.int64)
+    col_ptr = np.concatenate([[0], np.cumsum(sn_s)]).astype(np.int64)
+    row_ptr = np.concatenate([[0], np.cumsum(sn_r)]).astype(np.int64)
+    vals, d_off, m_off, n_off = [], [], [], []
+    off = 0
+    for q in order:
+        rec = recs[q]
+        for key, lst in (("d", d_off), ("m", m_off), ("nmat", n_off)):
+            lst.append(off)
+            vals.append(rec[key].ravel())
+            off += rec[key].size
+    children = [[] for _ in recs]
+    for q in order:
+        if recs[q]["parent"] >= 0:
+            children[recs[q]["parent"]].append(q)
+    in_lists = [[] for _ in range(col_ptr[-1])]
+    out_lists = [[] for _ in range(row_ptr[-1])]
+    for q in order:
+        p = pos[q]
+        ck, rk = recs[q]["col_keys"], recs[q]["row_keys"]
+        for c in children[q]:
+            ckeys = recs[c]["row_keys"]
+            slots = row_ptr[pos[c]] + np.arange(ckeys.size)
+            at = np.minimum(np.searchsorted(ck, ckeys), ck.size - 1)
+            inside = ck[at] == ckeys
+            for w, slot in zip(at[inside], slots[inside]):
+                in_lists[col_ptr[p] + int(w)].append(int(slot))
+            if (~inside).any():
+                where = np.searchsorted(rk, ckeys[~inside])
+                if not np.array_equal(rk[np.minimum(where, rk.size - 1)], ckeys[~inside]):
+                    raise AssertionError("supernode tree violates R_c within C_p + R_p")
+                for w, slot in zip(where, slots[~inside]):
+                    out_lists[row_ptr[p] + int(w)].append(int(slot))
+
+    def flat(lists):
+        ptr = np.concatenate([[0], np.cumsum([len(x) for x in lists])]).astype(np.int64)
+        idx = np.asarray([v for x in lists for v in x], dtype=np.int64)
+        return ptr, idx
+
+    in_ptr, in_idx = flat(in_lists)
+    out_ptr, out_idx = flat(out_lists)
+    cat = (lambda xs: np.concatenate(xs).astype(np.int64) if xs else np.zeros(0, np.int64))
+    return CoarseFactor(n, level_ptr, sn_s, sn_r, col_ptr, cat([recs[q]["cols"] for q in order]),
+                        row_ptr, cat([recs[q]["rows"] for q in order]),
+                        np.asarray(d_off, np.int64), np.asarray(m_off, np.int64),
+                        np.asarray(n_off, np.int64),
+                        np.concatenate(vals) if vals else np.zeros(0), in_ptr, in_idx, out_ptr,
+                        out_idx)
+
+
 def build_coarse_factor(a0, perm: np.ndarray | None = None,
                         max_zero_frac: float = 0.3) -> CoarseFactor:
     """Supernodal partitioned inverse of A0 (CsrMatrix or dense ndarray)."""
@@ -161,112 +301,208 @@ def build_coarse_factor(a0, perm: np.ndarray | None = None,
     if perm is None:
         perm = make_ordering(a0, "nested_dissection").perm
     perm = np.asarray(perm, dtype=np.int64)
-    ap = np.ascontiguousarray(dense[np.ix_(perm, perm)])
-    lu = _lu_nopivot(ap)
-    if not np.all(np.isfinite(lu)) or np.any(np.diag(lu) == 0.0):
-        raise np.linalg.LinAlgError("coarse matrix is singular")
-    low = np.tril(lu, -1)
-    up = np.triu(lu, 1)
-    nz = (low != 0.0) | (up.T != 0.0)
-    del low, up
-    starts, _ = _supernodes(nz, max_zero_frac)
+    lu = _lu_nopivot(np.ascontiguousarray(dense[np.ix_(perm, perm)]))
+    # the reference's pivot test (lu_numeric: |u_ii| <= 1e-14 ||A||_inf),
+    # here in nested-dissection order
+    tol = 1e-14 * np.abs(dense).sum(axis=1).max(initial=0.0)
+    bad = np.flatnonzero(~(np.abs(np.diag(lu)) > tol))
+    if bad.size:
+        raise np.linalg.LinAlgError(f"pivot too small at row {int(perm[bad[0]])}")
+    try:
+        recs = _records_from_lu(lu, np.arange(n, dtype=np.int64), perm, max_zero_frac)
+    except np.linalg.LinAlgError as err:
+        raise np.linalg.LinAlgError("coarse matrix is singular") from err
+    return _assemble(recs, n)
+
+
+def _records_from_csr(lp, li, lv, up, ui, uv, keys, ids, max_zero_frac):
+    """Supernode records of one sparse LU (L strictly lower, unit diagonal
+    implied; U with the diagonal first), built from the patterns without any
+    dense n x n array (block sizes of C3's 512 elasticity blocks)."""
+    import scipy.linalg as sl
+    import scipy.sparse as sp
+    n = lp.size - 1
+    ln = sp.csr_matrix((np.ones(li.size), li, lp), shape=(n, n))
+    ustrict = sp.csr_matrix((np.ones(ui.size), ui, up), shape=(n, n))
+    ustrict.setdiag(0)
+    ustrict.eliminate_zeros()
+    S = (ln + ustrict.T).tocsc()          # strictly lower, symmetrized structure
+    S.sort_indices()
+    cptr, cidx = S.indptr, S.indices
+    cc = np.diff(cptr)
+    parent = np.where(cc > 0, cidx[np.minimum(cptr[:-1], cidx.size - 1)], -1)
+    nchild = np.bincount(parent[parent >= 0], minlength=n)
+    j = np.arange(1, n)
+    fund = (parent[:-1] == j) & (cc[:-1] == cc[1:] + 1) & (nchild[1:] == 1)
+    starts = np.concatenate([[0], j[~fund], [n]]).astype(np.int64)
     nsn = starts.size - 1
     sn_of = np.repeat(np.arange(nsn), np.diff(starts))
-    # supernode tree: R_k = rows below supernode k; parent = supernode of the
-    # first row. Extend-add needs R_c within C_p + R_p for every child c of p
-    # (true of the elimination tree; enforced here so numerically vanished
-    # entries cannot break it: missing rows join R_p as explicit zeros)
-    sn_rows = [np.flatnonzero(nz[starts[k + 1]:, starts[k]:starts[k + 1]].any(axis=1)) + starts[k + 1]
-               for k in range(nsn)]
-    del nz
-    sn_par = np.full(nsn, -1, dtype=np.int64)
-    for k in range(nsn):  # children precede parents (ND postorder)
-        rows = sn_rows[k]
+    cols_of = [np.arange(starts[k], starts[k + 1]) for k in range(nsn)]
+    rows_of = []
+    for k in range(nsn):
+        st = cidx[cptr[starts[k]]:cptr[starts[k] + 1]]
+        rows_of.append(st[st >= starts[k + 1]])
+    par = np.full(nsn, -1, dtype=np.int64)
+    for k in range(nsn):   # extend-add containment (see _records_from_lu)
+        rows = rows_of[k]
         if rows.size:
             p = sn_of[rows[0]]
-            sn_par[k] = p
+            par[k] = p
             above = rows[rows >= starts[p + 1]]
-            extra = np.setdiff1d(above, sn_rows[p], assume_unique=True)
+            extra = np.setdiff1d(above, rows_of[p], assume_unique=True)
             if extra.size:
-                sn_rows[p] = np.union1d(sn_rows[p], extra)
-    height = np.zeros(nsn, dtype=np.int64)
+                rows_of[p] = np.union1d(rows_of[p], extra)
+    rep = np.arange(nsn)
+    nnz_l = [int(cc[starts[k]:starts[k + 1]].sum()) for k in range(nsn)]
+    nch = np.bincount(par[par >= 0], minlength=nsn)   # live children
+
+    def find(k):
+        while rep[k] != k:
+            rep[k] = rep[rep[k]]
+            k = rep[k]
+        return k
+
     for k in range(nsn):
-        if sn_par[k] >= 0:
-            height[sn_par[k]] = max(height[sn_par[k]], height[k] + 1)
-    order = np.lexsort((np.arange(nsn), height))   # processing order, leaves first
-    pos_of = np.empty(nsn, dtype=np.int64)
-    pos_of[order] = np.arange(nsn)
-    level_ptr = np.searchsorted(height[order], np.arange(height.max() + 2)).astype(np.int64)
-    import scipy.linalg as sl
-    vals, d_off, m_off, n_off = [], [], [], []
-    col_ids, row_ids = [], []
-    sn_s = np.zeros(nsn, dtype=np.int64)
-    sn_r = np.zeros(nsn, dtype=np.int64)
-    off = 0
-    for q, k in enumerate(order):
-        c0, c1 = starts[k], starts[k + 1]
-        rows = sn_rows[k]
-        s, r = c1 - c0, rows.size
-        sn_s[q], sn_r[q] = s, r
-        blk = lu[c0:c1, c0:c1]
-        lkk = np.tril(blk, -1) + np.eye(s)
-        ukk = np.triu(blk)
+        if par[k] < 0:
+            continue
+        p = find(par[k])
+        sz = cols_of[k].size + cols_of[p].size
+        merge = sz <= RELAX
+        if not merge and cols_of[p][0] == cols_of[k][-1] + 1 and nch[p] == 1:
+            # single-child chain: merge while the dense block's explicit
+            # zeros stay bounded
+            rows = np.setdiff1d(np.union1d(rows_of[p], rows_of[k]), cols_of[p])
+            dense = sz * (sz - 1) / 2 + sz * rows.size
+            merge = dense > 0 and 1.0 - (nnz_l[k] + nnz_l[p]) / dense <= max_zero_frac
+        if merge:
+            cols_of[p] = np.union1d(cols_of[p], cols_of[k])
+            rows_of[p] = np.setdiff1d(np.union1d(rows_of[p], rows_of[k]), cols_of[p])
+            nnz_l[p] += nnz_l[k]
+            nch[p] += nch[k] - 1
+            rep[k] = p
+            cols_of[k] = rows_of[k] = None
+    alive = [k for k in range(nsn) if rep[k] == k]
+    newid = np.full(nsn, -1, dtype=np.int64)
+    newid[alive] = np.arange(len(alive))
+    par2 = np.full(len(alive), -1, dtype=np.int64)
+    for q, k in enumerate(alive):
+        if rows_of[k].size:
+            par2[q] = newid[find(sn_of[rows_of[k][0]])]
+    height = np.zeros(len(alive), dtype=np.int64)
+    for q in range(len(alive)):
+        if par2[q] >= 0:
+            height[par2[q]] = max(height[par2[q]], height[q] + 1)
+    # scatter every factor entry into its supernode's dense panels at once:
+    # L entry (i, j) -> supernode of column j, row i in C (D) or R (M);
+    # U entry (i, j) -> supernode of row i, column j in C (D) or R (N)
+    sn_col = np.empty(n, dtype=np.int64)      # alive supernode of each column
+    cpos = np.empty(n, dtype=np.int64)        # position inside its column set
+    for q, k in enumerate(alive):
+        sn_col[cols_of[k]] = q
+        cpos[cols_of[k]] = np.arange(cols_of[k].size)
+    nq = len(alive)
+    s_q = np.asarray([cols_of[k].size for k in alive], dtype=np.int64)
+    r_q = np.asarray([rows_of[k].size for k in alive], dtype=np.int64)
+    rkey = np.concatenate([q * n + rows_of[k] for q, k in enumerate(alive)]) if nq else \
+        np.zeros(0, np.int64)
+    rbase = np.concatenate([[0], np.cumsum(r_q)])
+    lpan = [np.zeros((s_q[q] + r_q[q], s_q[q])) for q in range(nq)]   # [L_CC; L_RC]
+    upan = [np.zeros((s_q[q], s_q[q] + r_q[q])) for q in range(nq)]   # [U_CC, U_CR]
+
+    def place(rr, cc_, vals, lower):
+        q = sn_col[cc_] if lower else sn_col[rr]
+        other = rr if lower else cc_
+        inc = sn_col[other] == q
+        rpos = np.searchsorted(rkey, q * n + other) - rbase[q]
+        # panel coordinates, then one sorted pass over the supernodes
+        prow = np.where(inc, cpos[other], s_q[q] + rpos) if lower else cpos[rr]
+        pcol = cpos[cc_] if lower else np.where(inc, cpos[other], s_q[q] + rpos)
+        o = np.argsort(q, kind="stable")
+        bounds = np.searchsorted(q[o], np.arange(nq + 1))
+        pan = lpan if lower else upan
+        for qq in range(nq):
+            sl_ = o[bounds[qq]:bounds[qq + 1]]
+            pan[qq][prow[sl_], pcol[sl_]] = vals[sl_]
+
+    place(np.repeat(np.arange(n), np.diff(lp)), li, lv, True)
+    place(np.repeat(np.arange(n), np.diff(up)), ui, uv, False)
+    if not np.all(np.isfinite(uv)):
+        raise np.linalg.LinAlgError("matrix is singular")
+    recs = []
+    for q, k in enumerate(alive):
+        s = s_q[q]
+        lkk = lpan[q][:s] + np.eye(s)
+        ukk = upan[q][:, :s]
+        if np.any(np.diag(ukk) == 0.0):
+            raise np.linalg.LinAlgError("matrix is singular")
         linv = sl.solve_triangular(lkk, np.eye(s), lower=True, unit_diagonal=True)
         uinv = sl.solve_triangular(ukk, np.eye(s), lower=False)
-        dblk = np.tril(linv, -1) + np.triu(uinv)
-        mk = lu[np.ix_(rows, np.arange(c0, c1))] @ linv if r else np.zeros((0, s))
-        nk = uinv @ lu[np.ix_(np.arange(c0, c1), rows)] if r else np.zeros((s, 0))
-        d_off.append(off)
-        vals.append(dblk.ravel())
-        off += s * s
-        m_off.append(off)
-        vals.append(mk.ravel())
-        off += r * s
-        n_off.append(off)
-        vals.append(nk.ravel())
-        off += s * r
-        col_ids.append(perm[c0:c1])
-        row_ids.append(perm[rows])
-    col_ptr = np.concatenate([[0], np.cumsum(sn_s)]).astype(np.int64)
-    row_ptr = np.concatenate([[0], np.cumsum(sn_r)]).astype(np.int64)
-    # extend-add lists: the update vector of supernode p (over R_p, at
-    # row_ptr[p] in the buffer) = M_p bt_p + its children's updates at R_p;
-    # bt_p = u[C_p] - its children's updates at C_p. Children in processing
-    # order, so every sum has a fixed order.
-    children = [[] for _ in range(nsn)]
-    for q, k in enumerate(order):
-        if sn_par[k] >= 0:
-            children[pos_of[sn_par[k]]].append(q)
-    in_lists = [[] for _ in range(col_ptr[-1])]
-    out_lists = [[] for _ in range(row_ptr[-1])]
-    for q, k in enumerate(order):
-        c0, c1 = starts[k], starts[k + 1]
-        rows_p = sn_rows[k]
-        for qc in children[q]:
-            rc = sn_rows[order[qc]]
-            slots = row_ptr[qc] + np.arange(rc.size)
-            in_c = rc < c1
-            for g, slot in zip(rc[in_c], slots[in_c]):
-                in_lists[col_ptr[q] + (g - c0)].append(slot)
-            if (~in_c).any():
-                where = np.searchsorted(rows_p, rc[~in_c])
-                if not np.array_equal(rows_p[np.minimum(where, rows_p.size - 1)], rc[~in_c]):
-                    raise AssertionError("supernode tree violates R_c within C_p + R_p")
-                for w, slot in zip(where, slots[~in_c]):
-                    out_lists[row_ptr[q] + w].append(slot)
+        cols, rows = cols_of[k], rows_of[k]
+        recs.append(dict(
+            level=int(height[q]), parent=int(par2[q]),
+            col_keys=keys[cols], row_keys=keys[rows], cols=ids[cols], rows=ids[rows],
+            d=np.tril(linv, -1) + np.triu(uinv),
+            m=lpan[q][s:] @ linv, nmat=uinv @ upan[q][:, s:]))
+    return recs
 
-    def flat(lists):
-        ptr = np.concatenate([[0], np.cumsum([len(x) for x in lists])]).astype(np.int64)
-        idx = np.asarray([v for x in lists for v in x], dtype=np.int64)
-        return ptr, idx
 
-    in_ptr, in_idx = flat(in_lists)
-    out_ptr, out_idx = flat(out_lists)
-    return CoarseFactor(n, level_ptr, sn_s, sn_r, col_ptr, np.concatenate(col_ids), row_ptr,
-                        np.concatenate(row_ids) if row_ids else np.zeros(0, np.int64),
-                        np.asarray(d_off, np.int64), np.asarray(m_off, np.int64),
-                        np.asarray(n_off, np.int64), np.concatenate(vals),
-                        in_ptr, in_idx, out_ptr, out_idx)
+def build_block_factors(blocks, max_zero_frac: float = 0.3, threads: int = 0) -> CoarseFactor:
+    """Partitioned inverses of many independent exact-LU local factors, one
+    batch (supernodes of every block merged by tree level), built by the
+    host runtime (libgdsw_host.so, threaded over blocks). `blocks` = list of
+    (base, l_ptr, l_idx, l_val, u_ptr, u_idx, u_val): each block's CSR
+    factors in its own (already ND-permuted) numbering -- L strictly lower
+    with unit diagonal, U with the diagonal first -- and its offset in the
+    concatenated block vector. `build_block_factors_py` is the numpy
+    restatement the tests compare it with."""
+    import os
+    from . import _host
+    if not threads:
+        threads = os.cpu_count() or 1
+    blocks = [(b[0], np.asarray(b[1], np.int64), np.asarray(b[2], np.int64),
+               np.asarray(b[3], np.float64), np.asarray(b[4], np.int64),
+               np.asarray(b[5], np.int64), np.asarray(b[6], np.float64)) for b in blocks]
+    try:
+        arrs = _host.partitioned_inverse(blocks, RELAX, max_zero_frac, threads)
+    except RuntimeError as err:
+        if "singular" in str(err):
+            raise np.linalg.LinAlgError(str(err)) from err
+        raise
+    (level_ptr, sn_s, sn_r, col_ptr, col_ids, row_ptr, row_ids, d_off, m_off, n_off, values,
+     in_ptr, in_idx, out_ptr, out_idx) = arrs
+    n = max((b[0] + b[1].size - 1 for b in blocks), default=0)
+    return CoarseFactor(n, level_ptr, sn_s, sn_r, col_ptr, col_ids, row_ptr, row_ids, d_off,
+                        m_off, n_off, values, in_ptr, in_idx, out_ptr, out_idx)
+
+
+def build_block_factors_py(blocks, max_zero_frac: float = 0.3, threads: int = 8) -> CoarseFactor:
+    """Partitioned inverses of many independent exact-LU local factors, one
+    batch (supernodes of every block merged by tree level). `blocks` = list
+    of (base, l_ptr, l_idx, l_val, u_ptr, u_idx, u_val): the block's CSR
+    factors in its own (already ND-permuted) numbering -- L strictly lower
+    with unit diagonal, U with the diagonal first -- and the block's offset
+    in the concatenated block vector."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(blk):
+        base, lp, li, lv, up, ui, uv = blk
+        idx = base + np.arange(lp.size - 1, dtype=np.int64)
+        return _records_from_csr(np.asarray(lp, np.int64), np.asarray(li, np.int64),
+                                 np.asarray(lv, np.float64), np.asarray(up, np.int64),
+                                 np.asarray(ui, np.int64), np.asarray(uv, np.float64), idx, idx,
+                                 max_zero_frac)
+
+    with ThreadPoolExecutor(max_workers=max(1, threads)) as ex:
+        per = list(ex.map(one, blocks))
+    recs = []
+    for rs in per:
+        shift = len(recs)
+        for r in rs:
+            if r["parent"] >= 0:
+                r["parent"] += shift
+        recs.extend(rs)
+    n = max((b[0] + b[1].size - 1 for b in blocks), default=0)
+    return _assemble(recs, n)
 
 
 # n_c from which the factored solve replaces the dense inverse GEMV
@@ -287,13 +523,17 @@ def dense_inverse(a0) -> np.ndarray:
     return np.linalg.inv(dense)
 
 
-def install(pre, a0) -> str:
-    """Give the device preconditioner `pre` its coarse solve for A0:
-    the factored partitioned inverse for large n_c, else the dense inverse.
-    Returns the kind installed."""
+def use_factor(n_c: int) -> bool:
     import os
     mode = os.environ.get("GDSW_COARSE_FACTOR", "auto")
-    if mode == "1" or (mode != "0" and a0.nrows >= FACTOR_MIN_NC):
+    return mode == "1" or (mode != "0" and n_c >= FACTOR_MIN_NC)
+
+
+def install(pre, a0) -> str:
+    """Give the device preconditioner `pre` its coarse solve for A0:
+    the factored partitioned inverse for large n_c (its pivot-free LU is
+    the pivot check there), else the dense inverse. Returns the kind."""
+    if use_factor(a0.nrows):
         pre.set_coarse_factor(build_coarse_factor(a0))
         return "factor"
     pre.set_coarse_inverse(dense_inverse(a0))

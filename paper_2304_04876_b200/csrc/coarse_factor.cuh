@@ -56,10 +56,13 @@ __device__ __forceinline__ T cf_dot(const T* __restrict__ row, const T* vec, int
   return warp_sum((a0 + a1) + (a2 + a3));
 }
 
-template <typename T>
+// input u indexed by the solve's own vector index, or through gmap (the
+// local solves read the global residual r at gmap[k], rounded once to T)
+template <typename T, typename TI>
 __global__ void __launch_bounds__(CF_THREADS) k_cf_forward(CoarseFactorDev F, const int2* __restrict__ tasks,
-                                                           const T* __restrict__ vals, const T* __restrict__ u,
-                                                           T* __restrict__ y, T* __restrict__ cbuf) {
+                                                           const T* __restrict__ vals, const TI* __restrict__ u,
+                                                           const int32_t* __restrict__ gmap, T* __restrict__ y,
+                                                           T* __restrict__ cbuf) {
   extern __shared__ __align__(16) unsigned char cf_sm[];
   T* bt = reinterpret_cast<T*>(cf_sm);
   const int2 tk = tasks[blockIdx.x];
@@ -68,7 +71,8 @@ __global__ void __launch_bounds__(CF_THREADS) k_cf_forward(CoarseFactorDev F, co
   const int32_t* cols = F.col_ids + F.col_ptr[k];
   const int32_t cb = F.col_ptr[k];
   for (int i = threadIdx.x; i < s; i += CF_THREADS) {
-    T acc = u[cols[i]];
+    const int32_t c = cols[i];
+    T acc = (T)u[gmap ? gmap[c] : c];
     for (int32_t p = F.in_ptr[cb + i]; p < F.in_ptr[cb + i + 1]; ++p) acc -= cbuf[F.in_idx[p]];
     bt[i] = acc;
   }

@@ -564,6 +564,22 @@ extern "C" int gdsw_plan_destroy(gdsw_plan* p) {
 // ===========================================================================
 // numeric preconditioner
 // ===========================================================================
+// device copy of a supernodal partitioned inverse (coarse_factor.cuh)
+struct FactorBuf {
+  bool on = false;
+  DBuf<int32_t> sn_s, sn_r, col_ptr, col_ids, row_ptr, row_ids, in_ptr, in_idx, out_ptr, out_idx;
+  DBuf<int64_t> d_off, m_off, n_off;
+  DBuf<int2> tasks;
+  std::vector<int32_t> fwd_ptr, bwd_ptr;  // per level: task ranges (forward, backward)
+  std::vector<size_t> fwd_smem, bwd_smem;
+  DBuf<char> vals, ybuf, cbuf;
+  int64_t bytes = 0, n_launch = 0;
+  CoarseFactorDev dev() const {
+    return CoarseFactorDev{sn_s.p, sn_r.p, col_ptr.p, col_ids.p, row_ptr.p, row_ids.p,
+                           d_off.p, m_off.p, n_off.p, in_ptr.p, in_idx.p, out_ptr.p, out_idx.p};
+  }
+};
+
 struct gdsw_precond {
   gdsw_plan* plan = nullptr;
   std::unique_ptr<CoarsePlan> cp;
@@ -582,20 +598,9 @@ struct gdsw_precond {
   DBuf<char> panel32;              // f32 copy when dtype == F32
   DBuf<char> pgr_val, pgt_val, ainv;
   // factored coarse solve (coarse_factor.cuh); used instead of ainv when set
-  struct CoarseFactorBuf {
-    bool on = false;
-    DBuf<int32_t> sn_s, sn_r, col_ptr, col_ids, row_ptr, row_ids, in_ptr, in_idx, out_ptr, out_idx;
-    DBuf<int64_t> d_off, m_off, n_off;
-    DBuf<int2> tasks;
-    std::vector<int32_t> fwd_ptr, bwd_ptr;  // per level: task ranges (forward, backward)
-    std::vector<size_t> fwd_smem, bwd_smem;
-    DBuf<char> vals, ybuf, cbuf;
-    int64_t bytes = 0;
-    CoarseFactorDev dev() const {
-      return CoarseFactorDev{sn_s.p, sn_r.p, col_ptr.p, col_ids.p, row_ptr.p, row_ids.p,
-                             d_off.p, m_off.p, n_off.p, in_ptr.p, in_idx.p, out_ptr.p, out_idx.p};
-    }
-  } cf;
+  FactorBuf cf;
+  // factored exact-LU local solves (same kernels, every block in one batch)
+  FactorBuf lf;
   DBuf<char> xb, x1, x2, x3, pdot, cu, cv;
   // recursive: a GMRES solve holds it for its whole duration and its
   // eager passes re-enter precond_apply
@@ -846,6 +851,26 @@ T* levelset_solve(gdsw_precond* m, const double* r, cudaStream_t s) {
   return y;
 }
 
+// x = A^-1 u by a supernodal partitioned inverse: one launch per tree level
+// forward (leaves first), then one per level backward (root first)
+template <typename T, typename TI>
+void factor_solve(const FactorBuf& F, const TI* u, const int32_t* gmap, T* x, cudaStream_t s) {
+  const CoarseFactorDev D = F.dev();
+  const int nl = (int)F.fwd_smem.size();
+  for (int l = 0; l < nl; ++l) {
+    const int32_t t0 = F.fwd_ptr[l], nt = F.fwd_ptr[l + 1] - t0;
+    k_cf_forward<T, TI><<<nt, CF_THREADS, F.fwd_smem[l], s>>>(D, F.tasks.p + t0, (const T*)F.vals.p, u, gmap,
+                                                             (T*)F.ybuf.p, (T*)F.cbuf.p);
+    CK_LAUNCH();
+  }
+  for (int l = nl - 1; l >= 0; --l) {
+    const int32_t t0 = F.bwd_ptr[l], nt = F.bwd_ptr[l + 1] - t0;
+    k_cf_backward<T><<<nt, CF_THREADS, F.bwd_smem[l], s>>>(D, F.tasks.p + t0, (const T*)F.vals.p,
+                                                          (const T*)F.ybuf.p, x);
+    CK_LAUNCH();
+  }
+}
+
 template <typename T>
 T* local_solve(gdsw_precond* m, const double* r, int jacobi_iters, cudaStream_t s) {
   gdsw_plan* P = m->plan;
@@ -867,6 +892,13 @@ T* local_solve(gdsw_precond* m, const double* r, int jacobi_iters, cudaStream_t 
       return d16 ? jacobi_solve<T, false, true, true>(m, r, it, s) : jacobi_solve<T, false, false, true>(m, r, it, s);
     return d16 ? jacobi_solve<T, false, true, false>(m, r, it, s) : jacobi_solve<T, false, false, false>(m, r, it, s);
   }
+  if (m->lf.on) {
+    // exact LU: supernodal partitioned inverses of every block
+    ProfScope ps("factor_local", s, (double)m->lf.bytes + P->n_loc * 12.0);
+    T* y = (T*)m->x1.p;
+    factor_solve<T, double>(m->lf, r, P->gmap.p, y, s);
+    return y;
+  }
   return levelset_solve<T>(m, r, s);
 }
 
@@ -882,22 +914,8 @@ void coarse_solve(gdsw_precond* m, cudaStream_t cs) {
     CK_LAUNCH();
     return;
   }
-  auto& F = m->cf;
-  ProfScope ps("coarse_solve", cs, (double)F.bytes);
-  const CoarseFactorDev D = F.dev();
-  const int nl = (int)F.fwd_smem.size();
-  for (int l = 0; l < nl; ++l) {
-    const int32_t t0 = F.fwd_ptr[l], nt = F.fwd_ptr[l + 1] - t0;
-    k_cf_forward<T><<<nt, CF_THREADS, F.fwd_smem[l], cs>>>(D, F.tasks.p + t0, (const T*)F.vals.p,
-                                                          (const T*)m->cu.p, (T*)F.ybuf.p, (T*)F.cbuf.p);
-    CK_LAUNCH();
-  }
-  for (int l = nl - 1; l >= 0; --l) {
-    const int32_t t0 = F.bwd_ptr[l], nt = F.bwd_ptr[l + 1] - t0;
-    k_cf_backward<T><<<nt, CF_THREADS, F.bwd_smem[l], cs>>>(D, F.tasks.p + t0, (const T*)F.vals.p,
-                                                           (const T*)F.ybuf.p, (T*)m->cv.p);
-    CK_LAUNCH();
-  }
+  ProfScope ps("coarse_solve", cs, (double)m->cf.bytes);
+  factor_solve<T, T>(m->cf, (const T*)m->cu.p, nullptr, (T*)m->cv.p, cs);
 }
 
 template <typename T>
@@ -1492,74 +1510,90 @@ int gdsw_precond_set_coarse_inverse(gdsw_precond* m, const double* a0inv) {
   });
 }
 
+// upload a host partitioned inverse (gdsw_coarse_factor) into F in the
+// precond dtype; tasks are CF_ROWS-row tiles of each supernode's stacked
+// rows (forward: s + r, backward: s)
+static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype, size_t es) {
+  const int nsn = f->n_sn, nl = f->n_levels;
+  auto i32 = [](const int64_t* a, size_t n) { return to_i32(a, n); };
+  F.sn_s.upload(i32(f->sn_s, nsn));
+  F.sn_r.upload(i32(f->sn_r, nsn));
+  F.col_ptr.upload(i32(f->col_ptr, nsn + 1));
+  F.row_ptr.upload(i32(f->row_ptr, nsn + 1));
+  F.col_ids.upload(i32(f->col_ids, f->col_ptr[nsn]));
+  F.row_ids.upload(i32(f->row_ids, f->row_ptr[nsn]));
+  const int64_t ncol = f->col_ptr[nsn], nrow = f->row_ptr[nsn];
+  F.in_ptr.upload(i32(f->in_ptr, ncol + 1));
+  F.in_idx.upload(i32(f->in_idx, f->in_ptr[ncol]));
+  F.out_ptr.upload(i32(f->out_ptr, nrow + 1));
+  F.out_idx.upload(i32(f->out_idx, f->out_ptr[nrow]));
+  F.d_off.upload(f->d_off, nsn);
+  F.m_off.upload(f->m_off, nsn);
+  F.n_off.upload(f->n_off, nsn);
+  std::vector<int2> tasks;
+  F.fwd_ptr.assign(1, 0);
+  F.fwd_smem.assign(nl, 0);
+  F.bwd_smem.assign(nl, 0);
+  int64_t bytes = 0;
+  for (int l = 0; l < nl; ++l) {
+    for (int64_t k = f->level_ptr[l]; k < f->level_ptr[l + 1]; ++k) {
+      const int64_t s = f->sn_s[k], r = f->sn_r[k];
+      for (int64_t q = 0; q < s + r; q += CF_ROWS) tasks.push_back(make_int2((int)k, (int)q));
+      F.fwd_smem[l] = std::max(F.fwd_smem[l], (size_t)s * es);
+      bytes += (s * (s - 1) / 2 + r * s) * (int64_t)es;
+    }
+    F.fwd_ptr.push_back((int32_t)tasks.size());
+  }
+  F.bwd_ptr.assign(1, (int32_t)tasks.size());
+  for (int l = 0; l < nl; ++l) {
+    for (int64_t k = f->level_ptr[l]; k < f->level_ptr[l + 1]; ++k) {
+      const int64_t s = f->sn_s[k], r = f->sn_r[k];
+      for (int64_t q = 0; q < s; q += CF_ROWS) tasks.push_back(make_int2((int)k, (int)q));
+      F.bwd_smem[l] = std::max(F.bwd_smem[l], (size_t)(s + r) * es);
+      bytes += (s * (s + 1) / 2 + r * s) * (int64_t)es;
+    }
+    F.bwd_ptr.push_back((int32_t)tasks.size());
+  }
+  size_t smax = 0;
+  for (int l = 0; l < nl; ++l) smax = std::max({smax, F.fwd_smem[l], F.bwd_smem[l]});
+  require(smax <= 200 * 1024, "partitioned-inverse supernode too large for shared memory");
+  F.tasks.upload(tasks);
+  F.bytes = bytes;
+  F.n_launch = 2 * nl;
+  with_dtype(dtype, [&](auto tag) {
+    using T = decltype(tag);
+    std::vector<double> h(f->values, f->values + f->n_values);
+    upload_cast<T>(F.vals, h);
+    F.ybuf.alloc((size_t)f->n * sizeof(T));
+    F.cbuf.alloc((size_t)std::max<int64_t>(nrow, 1) * sizeof(T));
+    if (smax > 48 * 1024) {
+      CK(cudaFuncSetAttribute(k_cf_forward<T, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+      CK(cudaFuncSetAttribute(k_cf_forward<T, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+      CK(cudaFuncSetAttribute(k_cf_backward<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+    }
+  });
+  F.on = true;
+}
+
 int gdsw_precond_set_coarse_factor(gdsw_precond* m, const gdsw_coarse_factor* f) {
   return guarded([&] {
     require(m->cp != nullptr, "preconditioner has no coarse structure");
     require(f->n == m->cp->n_c, "coarse factor dimension mismatch");
-    auto& F = m->cf;
-    const int nsn = f->n_sn, nl = f->n_levels;
-    auto i32 = [](const int64_t* a, size_t n) { return to_i32(a, n); };
-    F.sn_s.upload(i32(f->sn_s, nsn));
-    F.sn_r.upload(i32(f->sn_r, nsn));
-    F.col_ptr.upload(i32(f->col_ptr, nsn + 1));
-    F.row_ptr.upload(i32(f->row_ptr, nsn + 1));
-    F.col_ids.upload(i32(f->col_ids, f->col_ptr[nsn]));
-    F.row_ids.upload(i32(f->row_ids, f->row_ptr[nsn]));
-    const int64_t ncol = f->col_ptr[nsn], nrow = f->row_ptr[nsn];
-    F.in_ptr.upload(i32(f->in_ptr, ncol + 1));
-    F.in_idx.upload(i32(f->in_idx, f->in_ptr[ncol]));
-    F.out_ptr.upload(i32(f->out_ptr, nrow + 1));
-    F.out_idx.upload(i32(f->out_idx, f->out_ptr[nrow]));
-    F.d_off.upload(f->d_off, nsn);
-    F.m_off.upload(f->m_off, nsn);
-    F.n_off.upload(f->n_off, nsn);
-    // tasks: forward levels (CF_ROWS-row tiles of the stacked s + r rows),
-    // then backward levels (tiles of the s rows)
-    std::vector<int2> tasks;
-    F.fwd_ptr.assign(1, 0);
-    F.bwd_ptr.clear();
-    F.fwd_smem.assign(nl, 0);
-    F.bwd_smem.assign(nl, 0);
-    int64_t bytes = 0;
-    const size_t es = m->es;
-    for (int l = 0; l < nl; ++l) {
-      for (int64_t k = f->level_ptr[l]; k < f->level_ptr[l + 1]; ++k) {
-        const int64_t s = f->sn_s[k], r = f->sn_r[k];
-        for (int64_t q = 0; q < s + r; q += CF_ROWS) tasks.push_back(make_int2((int)k, (int)q));
-        F.fwd_smem[l] = std::max(F.fwd_smem[l], (size_t)s * es);
-        bytes += (s * (s - 1) / 2 + r * s) * (int64_t)es;
-      }
-      F.fwd_ptr.push_back((int32_t)tasks.size());
-    }
-    F.bwd_ptr.assign(1, (int32_t)tasks.size());
-    for (int l = 0; l < nl; ++l) {
-      for (int64_t k = f->level_ptr[l]; k < f->level_ptr[l + 1]; ++k) {
-        const int64_t s = f->sn_s[k], r = f->sn_r[k];
-        for (int64_t q = 0; q < s; q += CF_ROWS) tasks.push_back(make_int2((int)k, (int)q));
-        F.bwd_smem[l] = std::max(F.bwd_smem[l], (size_t)(s + r) * es);
-        bytes += (s * (s + 1) / 2 + r * s) * (int64_t)es;
-      }
-      F.bwd_ptr.push_back((int32_t)tasks.size());
-    }
-    size_t smax = 0;
-    for (int l = 0; l < nl; ++l) smax = std::max({smax, F.fwd_smem[l], F.bwd_smem[l]});
-    require(smax <= 200 * 1024, "coarse factor supernode too large for shared memory");
-    F.tasks.upload(tasks);
-    F.bytes = bytes;
-    with_dtype(m->dtype, [&](auto tag) {
-      using T = decltype(tag);
-      std::vector<double> h(f->values, f->values + f->n_values);
-      upload_cast<T>(F.vals, h);
-      F.ybuf.alloc((size_t)f->n * sizeof(T));
-      F.cbuf.alloc((size_t)std::max<int64_t>(f->row_ptr[nsn], 1) * sizeof(T));
-      if (smax > 48 * 1024) {
-        CK(cudaFuncSetAttribute(k_cf_forward<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
-        CK(cudaFuncSetAttribute(k_cf_backward<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
-      }
-    });
-    F.on = true;
+    install_factor(m->cf, f, m->dtype, m->es);
     m->ainv.release();
     m->has_ainv = true;
+    m->drop_graphs();
+  });
+}
+
+int gdsw_precond_set_local_factor(gdsw_precond* m, const gdsw_coarse_factor* f) {
+  return guarded([&] {
+    require(f == nullptr || f->n == m->plan->n_loc, "local factor dimension mismatch");
+    if (f == nullptr) {
+      m->lf = FactorBuf{};
+    } else {
+      install_factor(m->lf, f, m->dtype, m->es);
+    }
     m->drop_graphs();
   });
 }

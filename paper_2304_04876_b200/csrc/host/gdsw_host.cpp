@@ -912,3 +912,369 @@ int gh_classify_interface(int64_t n_nodes, const int64_t* g_ptr, const int64_t* 
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// supernodal partitioned inverses of exact-LU factors (the device solve of
+// coarse_factor.cuh; Python restatement: coarse_factor._records_from_csr and
+// _assemble, which the tests compare against this)
+// ===========================================================================
+#include <atomic>
+#include <iterator>
+#include <thread>
+
+namespace {
+
+inline void require_host(bool ok, const char* msg) {
+  if (!ok) throw std::runtime_error(msg);
+}
+
+struct PinvSn {
+  i64 level = 0, parent = -1;
+  VI cols, rows;  // block-local ND positions, ascending
+  std::vector<double> d, m, nm;
+};
+
+// dense row-major helpers
+void tri_inv_unit_lower(i64 s, const std::vector<double>& a, std::vector<double>& inv) {
+  // a: s x s, strictly lower part used (unit diagonal)
+  inv.assign((size_t)s * s, 0.0);
+  for (i64 j = 0; j < s; ++j) {
+    inv[j * s + j] = 1.0;
+    for (i64 i = j + 1; i < s; ++i) {
+      double acc = 0.0;
+      for (i64 k = j; k < i; ++k) acc += a[i * s + k] * inv[k * s + j];
+      inv[i * s + j] = -acc;
+    }
+  }
+}
+
+void tri_inv_upper(i64 s, const std::vector<double>& a, std::vector<double>& inv) {
+  inv.assign((size_t)s * s, 0.0);
+  for (i64 j = s - 1; j >= 0; --j) {
+    inv[j * s + j] = 1.0 / a[j * s + j];
+    for (i64 i = j - 1; i >= 0; --i) {
+      double acc = 0.0;
+      for (i64 k = i + 1; k <= j; ++k) acc += a[i * s + k] * inv[k * s + j];
+      inv[i * s + j] = -acc / a[i * s + i];
+    }
+  }
+}
+
+std::vector<PinvSn> pinv_block(i64 n, const i64* lp, const i64* li, const double* lv, const i64* up,
+                               const i64* ui, const double* uv, i64 relax, double zf) {
+  // strictly lower symmetrized column structure
+  std::vector<VI> col(n);
+  for (i64 i = 0; i < n; ++i)
+    for (i64 p = lp[i]; p < lp[i + 1]; ++p) col[li[p]].push_back(i);
+  for (i64 j = 0; j < n; ++j)
+    for (i64 p = up[j]; p < up[j + 1]; ++p)
+      if (ui[p] > j) col[j].push_back(ui[p]);
+  VI cc(n), parent(n, -1);
+  for (i64 j = 0; j < n; ++j) {
+    std::sort(col[j].begin(), col[j].end());
+    col[j].erase(std::unique(col[j].begin(), col[j].end()), col[j].end());
+    cc[j] = (i64)col[j].size();
+    if (cc[j]) parent[j] = col[j][0];
+  }
+  VI nchild(n, 0);
+  for (i64 j = 0; j < n; ++j)
+    if (parent[j] >= 0) nchild[parent[j]]++;
+  VI starts{0};
+  for (i64 j = 1; j < n; ++j) {
+    const bool fund = parent[j - 1] == j && cc[j - 1] == cc[j] + 1 && nchild[j] == 1;
+    if (!fund) starts.push_back(j);
+  }
+  starts.push_back(n);
+  const i64 nsn = (i64)starts.size() - 1;
+  VI sn_of(n);
+  for (i64 k = 0; k < nsn; ++k)
+    for (i64 j = starts[k]; j < starts[k + 1]; ++j) sn_of[j] = k;
+  std::vector<VI> cols(nsn), rows(nsn);
+  VI nnz_l(nsn, 0);
+  for (i64 k = 0; k < nsn; ++k) {
+    for (i64 j = starts[k]; j < starts[k + 1]; ++j) {
+      cols[k].push_back(j);
+      nnz_l[k] += cc[j];
+    }
+    for (i64 r : col[starts[k]])
+      if (r >= starts[k + 1]) rows[k].push_back(r);
+  }
+  col.clear();
+  col.shrink_to_fit();
+  auto set_union = [](const VI& a, const VI& b) {
+    VI o;
+    o.reserve(a.size() + b.size());
+    std::set_union(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(o));
+    return o;
+  };
+  auto set_diff = [](const VI& a, const VI& b) {
+    VI o;
+    std::set_difference(a.begin(), a.end(), b.begin(), b.end(), std::back_inserter(o));
+    return o;
+  };
+  VI par(nsn, -1);
+  for (i64 k = 0; k < nsn; ++k) {  // extend-add containment
+    if (rows[k].empty()) continue;
+    const i64 p = sn_of[rows[k][0]];
+    par[k] = p;
+    VI above;
+    for (i64 r : rows[k])
+      if (r >= starts[p + 1]) above.push_back(r);
+    VI extra = set_diff(above, rows[p]);
+    if (!extra.empty()) rows[p] = set_union(rows[p], extra);
+  }
+  VI rep(nsn), nch(nsn, 0);
+  std::iota(rep.begin(), rep.end(), 0);
+  for (i64 k = 0; k < nsn; ++k)
+    if (par[k] >= 0) nch[par[k]]++;
+  auto find = [&](i64 k) {
+    while (rep[k] != k) {
+      rep[k] = rep[rep[k]];
+      k = rep[k];
+    }
+    return k;
+  };
+  for (i64 k = 0; k < nsn; ++k) {
+    if (par[k] < 0) continue;
+    const i64 p = find(par[k]);
+    const i64 sz = (i64)(cols[k].size() + cols[p].size());
+    bool merge = sz <= relax;
+    VI mrows;
+    if (!merge && cols[p][0] == cols[k].back() + 1 && nch[p] == 1) {
+      mrows = set_diff(set_union(rows[p], rows[k]), set_union(cols[p], cols[k]));
+      const double dense = (double)sz * (sz - 1) / 2.0 + (double)sz * mrows.size();
+      merge = dense > 0 && 1.0 - (double)(nnz_l[k] + nnz_l[p]) / dense <= zf;
+    }
+    if (merge) {
+      cols[p] = set_union(cols[p], cols[k]);
+      rows[p] = set_diff(set_union(rows[p], rows[k]), cols[p]);
+      nnz_l[p] += nnz_l[k];
+      nch[p] += nch[k] - 1;
+      rep[k] = p;
+      VI().swap(cols[k]);
+      VI().swap(rows[k]);
+    }
+  }
+  VI alive, newid(nsn, -1);
+  for (i64 k = 0; k < nsn; ++k)
+    if (rep[k] == k) {
+      newid[k] = (i64)alive.size();
+      alive.push_back(k);
+    }
+  const i64 nq = (i64)alive.size();
+  std::vector<PinvSn> out(nq);
+  VI sn_col(n), cpos(n);
+  for (i64 q = 0; q < nq; ++q) {
+    const i64 k = alive[q];
+    out[q].cols = std::move(cols[k]);
+    out[q].rows = std::move(rows[k]);
+    for (size_t t = 0; t < out[q].cols.size(); ++t) {
+      sn_col[out[q].cols[t]] = q;
+      cpos[out[q].cols[t]] = (i64)t;
+    }
+  }
+  for (i64 q = 0; q < nq; ++q)
+    if (!out[q].rows.empty()) out[q].parent = newid[find(sn_of[out[q].rows[0]])];
+  for (i64 q = 0; q < nq; ++q)
+    if (out[q].parent >= 0) out[out[q].parent].level = std::max(out[out[q].parent].level, out[q].level + 1);
+  // panels [L_CC; L_RC] ((s + r) x s) and [U_CC, U_CR] (s x (s + r))
+  std::vector<std::vector<double>> lpan(nq), upan(nq);
+  for (i64 q = 0; q < nq; ++q) {
+    const i64 s = (i64)out[q].cols.size(), r = (i64)out[q].rows.size();
+    lpan[q].assign((size_t)(s + r) * s, 0.0);
+    upan[q].assign((size_t)s * (s + r), 0.0);
+  }
+  auto rpos = [&](i64 q, i64 g) {
+    const VI& R = out[q].rows;
+    auto it = std::lower_bound(R.begin(), R.end(), g);
+    require_host(it != R.end() && *it == g, "partitioned inverse: row outside its supernode");
+    return (i64)(it - R.begin());
+  };
+  for (i64 i = 0; i < n; ++i)
+    for (i64 p = lp[i]; p < lp[i + 1]; ++p) {
+      const i64 j = li[p], q = sn_col[j], s = (i64)out[q].cols.size();
+      const i64 row = sn_col[i] == q ? cpos[i] : s + rpos(q, i);
+      lpan[q][row * s + cpos[j]] = lv[p];
+    }
+  for (i64 i = 0; i < n; ++i)
+    for (i64 p = up[i]; p < up[i + 1]; ++p) {
+      const i64 j = ui[p], q = sn_col[i], s = (i64)out[q].cols.size(), r = (i64)out[q].rows.size();
+      const i64 c = sn_col[j] == q ? cpos[j] : s + rpos(q, j);
+      upan[q][cpos[i] * (s + r) + c] = uv[p];
+    }
+  std::vector<double> lkk, ukk, linv, uinv;
+  for (i64 q = 0; q < nq; ++q) {
+    const i64 s = (i64)out[q].cols.size(), r = (i64)out[q].rows.size();
+    lkk.assign((size_t)s * s, 0.0);
+    ukk.assign((size_t)s * s, 0.0);
+    for (i64 i = 0; i < s; ++i)
+      for (i64 j = 0; j < s; ++j) {
+        lkk[i * s + j] = lpan[q][i * s + j];
+        ukk[i * s + j] = upan[q][i * (s + r) + j];
+      }
+    for (i64 i = 0; i < s; ++i)
+      require_host(ukk[i * s + i] != 0.0 && std::isfinite(ukk[i * s + i]), "matrix is singular");
+    tri_inv_unit_lower(s, lkk, linv);
+    tri_inv_upper(s, ukk, uinv);
+    PinvSn& o = out[q];
+    o.d.assign((size_t)s * s, 0.0);
+    for (i64 i = 0; i < s; ++i)
+      for (i64 j = 0; j < s; ++j) o.d[i * s + j] = j < i ? linv[i * s + j] : uinv[i * s + j];
+    // M = L_RC linv (r x s): row i of L_RC times linv (lower), k >= j
+    o.m.assign((size_t)r * s, 0.0);
+    for (i64 i = 0; i < r; ++i) {
+      const double* lr = &lpan[q][(s + i) * s];
+      double* mr = &o.m[i * s];
+      for (i64 k = 0; k < s; ++k) {
+        const double a = lr[k];
+        if (a == 0.0) continue;
+        const double* lk = &linv[k * s];
+        for (i64 j = 0; j <= k; ++j) mr[j] += a * lk[j];
+      }
+    }
+    // N = uinv U_CR (s x r)
+    o.nm.assign((size_t)s * r, 0.0);
+    for (i64 i = 0; i < s; ++i) {
+      double* nr = &o.nm[i * r];
+      for (i64 k = i; k < s; ++k) {
+        const double a = uinv[i * s + k];
+        if (a == 0.0) continue;
+        const double* ur = &upan[q][k * (s + r) + s];
+        for (i64 j = 0; j < r; ++j) nr[j] += a * ur[j];
+      }
+    }
+    std::vector<double>().swap(lpan[q]);
+    std::vector<double>().swap(upan[q]);
+  }
+  return out;
+}
+
+}  // namespace
+
+extern "C" int gh_partitioned_inverse(int64_t nblk, const int64_t* blk_n, const int64_t* blk_base,
+                                      const int64_t* lp_off, const int64_t* lnz_off, const int64_t* up_off,
+                                      const int64_t* unz_off, const int64_t* lp, const int64_t* li,
+                                      const double* lv, const int64_t* up, const int64_t* ui,
+                                      const double* uv, int64_t relax, double zero_frac, int64_t threads,
+                                      gh_result** res) {
+  GH_TRY({
+    std::vector<std::vector<PinvSn>> per(nblk);
+    std::vector<std::string> errs(nblk);
+    std::atomic<i64> next{0};
+    auto work = [&] {
+      for (;;) {
+        const i64 b = next.fetch_add(1);
+        if (b >= nblk) break;
+        try {
+          per[b] = pinv_block(blk_n[b], lp + lp_off[b], li + lnz_off[b], lv + lnz_off[b], up + up_off[b],
+                              ui + unz_off[b], uv + unz_off[b], relax, zero_frac);
+        } catch (const std::exception& e) {
+          errs[b] = e.what();
+        }
+      }
+    };
+    std::vector<std::thread> pool;
+    for (i64 t = 1; t < std::max<i64>(1, threads); ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+    for (i64 b = 0; b < nblk; ++b)
+      if (!errs[b].empty()) throw std::runtime_error("block " + std::to_string(b) + ": " + errs[b]);
+    // global records in (block, local) order; processing order by (level, that)
+    struct Ref { i64 b, q, g, level; };
+    std::vector<Ref> refs;
+    VI first(nblk + 1, 0);
+    for (i64 b = 0; b < nblk; ++b) {
+      first[b + 1] = first[b] + (i64)per[b].size();
+      for (i64 q = 0; q < (i64)per[b].size(); ++q) refs.push_back({b, q, first[b] + q, per[b][q].level});
+    }
+    const i64 nsn = (i64)refs.size();
+    std::vector<Ref> ord(refs);
+    std::stable_sort(ord.begin(), ord.end(), [](const Ref& x, const Ref& y) { return x.level < y.level; });
+    VI pos(nsn);
+    for (i64 t = 0; t < nsn; ++t) pos[ord[t].g] = t;
+    i64 nlev = 0;
+    for (const Ref& r : ord) nlev = std::max(nlev, r.level + 1);
+    VI level_ptr(nlev + 1, 0), sn_s(nsn), sn_r(nsn), col_ptr(nsn + 1, 0), row_ptr(nsn + 1, 0);
+    for (const Ref& r : ord) level_ptr[r.level + 1]++;
+    for (i64 l = 0; l < nlev; ++l) level_ptr[l + 1] += level_ptr[l];
+    for (i64 t = 0; t < nsn; ++t) {
+      const PinvSn& o = per[ord[t].b][ord[t].q];
+      sn_s[t] = (i64)o.cols.size();
+      sn_r[t] = (i64)o.rows.size();
+      col_ptr[t + 1] = col_ptr[t] + sn_s[t];
+      row_ptr[t + 1] = row_ptr[t] + sn_r[t];
+    }
+    VI col_ids(col_ptr[nsn]), row_ids(row_ptr[nsn]), d_off(nsn), m_off(nsn), n_off(nsn);
+    i64 nval = 0;
+    for (i64 t = 0; t < nsn; ++t) {
+      const PinvSn& o = per[ord[t].b][ord[t].q];
+      const i64 base = blk_base[ord[t].b];
+      for (i64 c = 0; c < sn_s[t]; ++c) col_ids[col_ptr[t] + c] = base + o.cols[c];
+      for (i64 c = 0; c < sn_r[t]; ++c) row_ids[row_ptr[t] + c] = base + o.rows[c];
+      d_off[t] = nval;
+      nval += (i64)o.d.size();
+      m_off[t] = nval;
+      nval += (i64)o.m.size();
+      n_off[t] = nval;
+      nval += (i64)o.nm.size();
+    }
+    std::vector<double> vals((size_t)nval);
+    for (i64 t = 0; t < nsn; ++t) {
+      const PinvSn& o = per[ord[t].b][ord[t].q];
+      std::copy(o.d.begin(), o.d.end(), vals.begin() + d_off[t]);
+      std::copy(o.m.begin(), o.m.end(), vals.begin() + m_off[t]);
+      std::copy(o.nm.begin(), o.nm.end(), vals.begin() + n_off[t]);
+    }
+    // extend-add lists: children (processing order) of each supernode
+    std::vector<VI> children(nsn);
+    for (i64 t = 0; t < nsn; ++t) {
+      const PinvSn& o = per[ord[t].b][ord[t].q];
+      if (o.parent >= 0) children[pos[first[ord[t].b] + o.parent]].push_back(t);
+    }
+    std::vector<VI> in_l(col_ptr[nsn]), out_l(row_ptr[nsn]);
+    for (i64 t = 0; t < nsn; ++t) {
+      const PinvSn& o = per[ord[t].b][ord[t].q];
+      for (i64 c : children[t]) {
+        const PinvSn& oc = per[ord[c].b][ord[c].q];
+        for (i64 m = 0; m < (i64)oc.rows.size(); ++m) {
+          const i64 g = oc.rows[m], slot = row_ptr[c] + m;
+          auto it = std::lower_bound(o.cols.begin(), o.cols.end(), g);
+          if (it != o.cols.end() && *it == g) {
+            in_l[col_ptr[t] + (it - o.cols.begin())].push_back(slot);
+          } else {
+            auto jt = std::lower_bound(o.rows.begin(), o.rows.end(), g);
+            require_host(jt != o.rows.end() && *jt == g, "supernode tree violates R_c within C_p + R_p");
+            out_l[row_ptr[t] + (jt - o.rows.begin())].push_back(slot);
+          }
+        }
+      }
+    }
+    auto flat = [](const std::vector<VI>& lists, VI& ptr, VI& idx) {
+      ptr.assign(lists.size() + 1, 0);
+      for (size_t i = 0; i < lists.size(); ++i) ptr[i + 1] = ptr[i] + (i64)lists[i].size();
+      idx.clear();
+      idx.reserve(ptr.back());
+      for (const VI& l : lists) idx.insert(idx.end(), l.begin(), l.end());
+    };
+    VI in_ptr, in_idx, out_ptr, out_idx;
+    flat(in_l, in_ptr, in_idx);
+    flat(out_l, out_ptr, out_idx);
+    auto* r = new gh_result;
+    r->add(std::move(level_ptr));
+    r->add(std::move(sn_s));
+    r->add(std::move(sn_r));
+    r->add(std::move(col_ptr));
+    r->add(std::move(col_ids));
+    r->add(std::move(row_ptr));
+    r->add(std::move(row_ids));
+    r->add(std::move(d_off));
+    r->add(std::move(m_off));
+    r->add(std::move(n_off));
+    r->add(std::move(vals));
+    r->add(std::move(in_ptr));
+    r->add(std::move(in_idx));
+    r->add(std::move(out_ptr));
+    r->add(std::move(out_idx));
+    *res = r;
+  })
+}

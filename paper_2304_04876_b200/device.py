@@ -87,6 +87,7 @@ _SIGS = {
     "gdsw_precond_get_panels": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gdsw_precond_set_coarse_inverse": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gdsw_precond_set_coarse_factor": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gdsw_precond_set_local_factor": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gdsw_precond_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "gdsw_precond_local_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int,
                                            C.c_void_p]),
@@ -380,13 +381,27 @@ class Precond:
         a = np.ascontiguousarray(a0inv, dtype=np.float64)
         _ck(_lib.gdsw_precond_set_coarse_inverse(self.handle, _ptr(a)))
 
-    def set_coarse_factor(self, f):
-        """Factored coarse solve (coarse_factor.CoarseFactor)."""
+    @staticmethod
+    def _factor_desc(f):
         keep = {k: np.ascontiguousarray(getattr(f, k), dtype=np.int64) for k in _CF_ARRAYS}
         vals = np.ascontiguousarray(f.values, dtype=np.float64)
         d = _CoarseFactor(n=f.n, n_sn=f.n_sn, n_levels=f.n_levels, values=vals.ctypes.data,
                           n_values=vals.size, **{k: v.ctypes.data for k, v in keep.items()})
+        return d, (keep, vals)
+
+    def set_coarse_factor(self, f):
+        """Factored coarse solve (coarse_factor.CoarseFactor)."""
+        d, _keep = self._factor_desc(f)
         _ck(_lib.gdsw_precond_set_coarse_factor(self.handle, C.byref(d)))
+
+    def set_local_factor(self, f):
+        """Factored exact-LU local solves (coarse_factor.build_block_factors),
+        or None for the level-set path."""
+        if f is None:
+            _ck(_lib.gdsw_precond_set_local_factor(self.handle, None))
+            return
+        d, _keep = self._factor_desc(f)
+        _ck(_lib.gdsw_precond_set_local_factor(self.handle, C.byref(d)))
 
     def apply(self, r, z):
         _ck(_lib.gdsw_precond_apply(self.handle, _ptr(r), _ptr(z), stream_handle()))

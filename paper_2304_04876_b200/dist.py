@@ -189,6 +189,14 @@ class DistPreconditioner:
         own = _range_rows(sh.g0, sh.g1)
         self.a_own = device.DeviceCsr(extract_submatrix(a, own, ext))
 
+    @property
+    def a0_factorization(self):
+        """The reference's sparse LU of A0, built on first access when the
+        device solve uses the factored partitioned inverse."""
+        if callable(self._a0_fac):
+            self._a0_fac = self._a0_fac()
+        return self._a0_fac
+
     def _coarse(self, a, coarse_src, a_ext, a_ext_dev, dec, nullspace, config, single, group):
         sh = self.shard
         structure = dec.structure
@@ -243,12 +251,16 @@ class DistPreconditioner:
         a0 = self.pre.coarse_galerkin(a_own_src, n_c, self.layout)
         if single:
             a0 = convert_precision(a0, np.float32)
+        from .coarse_factor import install as _install_coarse
+        from .coarse_factor import use_factor
+        order = config.ordering
+        self._a0_fac = lambda: numeric_lu(a0, symbolic_lu(a0, make_ordering(a0, order)))
         try:
-            self.a0_factorization = numeric_lu(a0, symbolic_lu(a0, make_ordering(a0, config.ordering)))
+            if not use_factor(a0.nrows):  # the reference's pivot check
+                self._a0_fac = self._a0_fac()
+            _install_coarse(self.pre, a0)
         except np.linalg.LinAlgError as err:
             raise np.linalg.LinAlgError(f"coarse matrix is singular: {err}") from err
-        from .coarse_factor import install as _install_coarse
-        _install_coarse(self.pre, a0)
         self.a0 = a0
         self.phi_local = phi_ext
         self.column_map = column_map

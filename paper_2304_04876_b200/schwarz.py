@@ -291,8 +291,16 @@ class CoarseSolver:
                  column_map: list):
         self._phi, self._phi_t = phi, phi_t
         self.a0 = a0
-        self.a0_factorization = a0_factorization
+        self._a0_fac = a0_factorization
         self.column_map = column_map
+
+    @property
+    def a0_factorization(self) -> LocalFactorization:
+        """The reference's sparse LU of A0 (config.ordering); built on first
+        access when the device solve uses the factored partitioned inverse."""
+        if callable(self._a0_fac):
+            self._a0_fac = self._a0_fac()
+        return self._a0_fac
 
     @property
     def phi(self) -> CsrMatrix:
@@ -476,6 +484,9 @@ def setup_numeric(skeleton: PreconditionerSkeleton, a: CsrMatrix,
         pre.set_factors(_cat(lvs, value_dtype), _cat(uvs, value_dtype))
 
     tick("local factors")
+    if spec.method == "exact_lu" and _local_factor_pays(skeleton):
+        _install_local_factor(pre, plan, skeleton)
+        tick("local partitioned inverses")
     coarse = None
     if config.use_coarse:
         if nullspace is None:
@@ -493,13 +504,17 @@ def setup_numeric(skeleton: PreconditionerSkeleton, a: CsrMatrix,
         if single:
             phi = lambda: convert_precision(phi64(), np.float32)  # noqa: E731
             a0 = convert_precision(a0, np.float32)
+        from .coarse_factor import install as _install_coarse
+        from .coarse_factor import use_factor
+        a0_fac = _coarse_lu_thunk(a0, config.ordering)
         try:
-            a0_fac = numeric_lu(a0, symbolic_lu(a0, make_ordering(a0, config.ordering)))
+            if not use_factor(a0.nrows):
+                # the reference's pivot check (sparse LU with config.ordering)
+                a0_fac = a0_fac()
+                tick("A0 sparse LU (pivot check)")
+            kind = _install_coarse(pre, a0)
         except np.linalg.LinAlgError as err:
             raise np.linalg.LinAlgError(f"coarse matrix is singular: {err}") from err
-        tick("A0 sparse LU (pivot check)")
-        from .coarse_factor import install as _install_coarse
-        kind = _install_coarse(pre, a0)
         tick(f"coarse solve ({kind})")
         coarse = CoarseSolver(phi, None, a0, a0_fac, column_map)
 
@@ -509,6 +524,39 @@ def setup_numeric(skeleton: PreconditionerSkeleton, a: CsrMatrix,
         if f._l_values is None:
             f._source = (m, s)
     return m
+
+
+def _coarse_lu_thunk(a0, ordering):
+    return lambda: numeric_lu(a0, symbolic_lu(a0, make_ordering(a0, ordering)))
+
+
+def _local_factor_pays(skeleton) -> bool:
+    """Exact-LU blocks solve through supernodal partitioned inverses
+    (coarse_factor.build_block_factors): the nested-dissection elimination
+    tree's height (C1: 12 levels) replaces the level schedule's one-row
+    levels (C1: 492 per factor). GDSW_LOCAL_FACTOR=0 / =1 forces."""
+    import os
+    force = os.environ.get("GDSW_LOCAL_FACTOR", "")
+    if force in ("0", "1"):
+        return force == "1"
+    syms = skeleton.local_symbolics
+    fill = sum(s.l_idx.size + s.u_idx.size for s in syms)
+    return fill <= 2_000_000_000 and max(s.n for s in syms) <= 20_000
+
+
+def _install_local_factor(pre, plan, skeleton):
+    from .coarse_factor import build_block_factors
+    syms = skeleton.local_symbolics
+    lv, uv = pre.factors(plan.nnz_l, plan.nnz_u)
+    blocks, base, lo, uo = [], 0, 0, 0
+    for sym in syms:
+        nl, nu = sym.l_idx.size, sym.u_idx.size
+        blocks.append((base, sym.l_ptr, sym.l_idx, lv[lo:lo + nl], sym.u_ptr, sym.u_idx,
+                       uv[uo:uo + nu]))
+        base += sym.n
+        lo += nl
+        uo += nu
+    pre.set_local_factor(build_block_factors(blocks))
 
 
 def _setup_clock():
