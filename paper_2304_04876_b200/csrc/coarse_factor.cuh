@@ -20,9 +20,16 @@
 namespace gdsw {
 
 constexpr int CF_THREADS = 256;
-constexpr int CF_ROWS = 16;  // rows of a block per CTA task
+constexpr int CF_ROWS = 8;   // rows of a block per CTA task (one per warp)
 
 struct CoarseFactorDev {
+  // dataflow schedule (k_cf_dataflow): parent of each supernode, its
+  // children, and the readiness targets
+  const int32_t* parent;
+  const int32_t* child_ptr;
+  const int32_t* child_idx;
+  const int32_t* fwd_need;   // forward tiles of the children
+  const int32_t* bwd_need;   // own forward tiles + the parent's backward tiles
   const int32_t* sn_s;
   const int32_t* sn_r;
   const int32_t* col_ptr;
@@ -39,21 +46,24 @@ struct CoarseFactorDev {
 };
 
 // dot of a dense row segment [j0, j1) with a shared-memory vector: lanes
-// over the columns, four independent partial sums (loads in flight)
+// over the columns, eight independent partial sums (eight row loads in
+// flight per lane: one row per warp must keep HBM busy on its own when a
+// level holds few supernodes)
 template <typename T>
 __device__ __forceinline__ T cf_dot(const T* __restrict__ row, const T* vec, int j0, int j1, int lane) {
-  T a0 = T(0), a1 = T(0), a2 = T(0), a3 = T(0);
+  T a[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) a[u] = T(0);
   int j = j0 + lane;
-  for (; j + 96 < j1; j += 128) {
-    const T r0 = ldg_stream(row + j), r1 = ldg_stream(row + j + 32), r2 = ldg_stream(row + j + 64),
-            r3 = ldg_stream(row + j + 96);
-    a0 = fma(r0, vec[j], a0);
-    a1 = fma(r1, vec[j + 32], a1);
-    a2 = fma(r2, vec[j + 64], a2);
-    a3 = fma(r3, vec[j + 96], a3);
+  for (; j + 224 < j1; j += 256) {
+    T rr[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) rr[u] = ldg_stream(row + j + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) a[u] = fma(rr[u], vec[j + 32 * u], a[u]);
   }
-  for (; j < j1; j += 32) a0 = fma(ldg_stream(row + j), vec[j], a0);
-  return warp_sum((a0 + a1) + (a2 + a3));
+  for (; j < j1; j += 32) a[0] = fma(ldg_stream(row + j), vec[j], a[0]);
+  return warp_sum(((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
 }
 
 // input u indexed by the solve's own vector index, or through gmap (the
@@ -116,6 +126,126 @@ __global__ void __launch_bounds__(CF_THREADS) k_cf_backward(CoarseFactorDev F, c
     const T a = cf_dot(vals + F.d_off[k] + (int64_t)row * s, in, row, s, lane);
     const T b = cf_dot(vals + F.n_off[k] + (int64_t)row * r, in + s, 0, r, lane);
     if (lane == 0) x[cols[row]] = a - b;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// the whole solve in ONE launch: a persistent grid takes the tasks (forward
+// tiles leaves-first, then backward tiles root-first) from an atomic ticket
+// in order and runs each as soon as its inputs exist: a forward tile waits
+// for every forward tile of its children (their updates), a backward tile
+// for its own forward tiles (y) and every backward tile of its parent (x on
+// R_k; the parent waited for its own parent). Tiles signal with release
+// atomics on per-supernode counters. No level barriers, so independent
+// subtrees overlap. Tasks are taken in dependency order by resident CTAs,
+// so every awaited tile is already running: no deadlock. The last CTA to
+// leave resets the ticket and counters (graph-replay safe).
+struct CfSched {
+  unsigned* ticket;     // [0]: next task, [1]: CTAs done
+  int32_t* fwd_ready;   // per supernode
+  int32_t* bwd_ready;
+  int32_t n_fwd, n_tasks, n_sn;
+};
+
+__device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename T, typename TI>
+__global__ void __launch_bounds__(CF_THREADS) k_cf_dataflow(CoarseFactorDev F, CfSched S,
+                                                            const int2* __restrict__ tasks,
+                                                            const T* __restrict__ vals, const TI* __restrict__ u,
+                                                            const int32_t* __restrict__ gmap, T* __restrict__ y,
+                                                            T* __restrict__ cbuf, T* __restrict__ x) {
+  extern __shared__ __align__(16) unsigned char cf_sm[];
+  T* buf = reinterpret_cast<T*>(cf_sm);
+  __shared__ int32_t cur;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (;;) {
+    if (threadIdx.x == 0) cur = (int32_t)atomicAdd(S.ticket, 1u);
+    __syncthreads();
+    const int32_t t = cur;
+    if (t >= S.n_tasks) break;
+    const bool fwd = t < S.n_fwd;
+    const int2 tk = tasks[t];
+    const int k = tk.x, row0 = tk.y;
+    const int s = F.sn_s[k], r = F.sn_r[k];
+    const int32_t* cols = F.col_ids + F.col_ptr[k];
+    if (threadIdx.x == 0) {
+      const int32_t* ready = fwd ? S.fwd_ready + k : S.bwd_ready + k;
+      const int32_t need = fwd ? F.fwd_need[k] : F.bwd_need[k];
+      while (ld_acquire_gpu(ready) < need) __nanosleep(20);
+    }
+    __syncthreads();
+    if (fwd) {
+      const int32_t cb = F.col_ptr[k];
+      for (int i = threadIdx.x; i < s; i += CF_THREADS) {
+        const int32_t c = cols[i];
+        T acc = (T)u[gmap ? gmap[c] : c];
+        for (int32_t p = F.in_ptr[cb + i]; p < F.in_ptr[cb + i + 1]; ++p) acc -= __ldcg(cbuf + F.in_idx[p]);
+        buf[i] = acc;
+      }
+      __syncthreads();
+      for (int q = warp; q < CF_ROWS; q += CF_THREADS / 32) {
+        const int row = row0 + q;
+        if (row >= s + r) break;
+        if (row < s) {
+          const T acc = cf_dot(vals + F.d_off[k] + (int64_t)row * s, buf, 0, row, lane);
+          if (lane == 0) y[cols[row]] = acc + buf[row];
+        } else {
+          T acc = cf_dot(vals + F.m_off[k] + (int64_t)(row - s) * s, buf, 0, s, lane);
+          if (lane == 0) {
+            const int32_t g = F.row_ptr[k] + row - s;
+            for (int32_t p = F.out_ptr[g]; p < F.out_ptr[g + 1]; ++p) acc += __ldcg(cbuf + F.out_idx[p]);
+            cbuf[g] = acc;
+          }
+        }
+      }
+    } else {
+      const int32_t* rows = F.row_ids + F.row_ptr[k];
+      for (int i = threadIdx.x; i < s + r; i += CF_THREADS)
+        buf[i] = i < s ? __ldcg(y + cols[i]) : __ldcg(x + rows[i - s]);
+      __syncthreads();
+      for (int q = warp; q < CF_ROWS; q += CF_THREADS / 32) {
+        const int row = row0 + q;
+        if (row >= s) break;
+        const T a = cf_dot(vals + F.d_off[k] + (int64_t)row * s, buf, row, s, lane);
+        const T b = cf_dot(vals + F.n_off[k] + (int64_t)row * r, buf + s, 0, r, lane);
+        if (lane == 0) x[cols[row]] = a - b;
+      }
+    }
+    // publish: every thread's stores, then one release increment per
+    // dependent supernode
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (fwd) {
+        atomicAdd(S.bwd_ready + k, 1);
+        const int32_t p = F.parent[k];
+        if (p >= 0) atomicAdd(S.fwd_ready + p, 1);
+      } else {
+        for (int32_t c = F.child_ptr[k]; c < F.child_ptr[k + 1]; ++c) atomicAdd(S.bwd_ready + F.child_idx[c], 1);
+      }
+    }
+  }
+  // the last CTA out resets the schedule for the next solve
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(S.ticket + 1, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {
+    for (int32_t i = threadIdx.x; i < S.n_sn; i += CF_THREADS) {
+      S.fwd_ready[i] = 0;
+      S.bwd_ready[i] = 0;
+    }
+    if (threadIdx.x == 0) {
+      S.ticket[0] = 0u;
+      S.ticket[1] = 0u;
+    }
   }
 }
 

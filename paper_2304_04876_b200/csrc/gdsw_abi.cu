@@ -569,13 +569,18 @@ struct FactorBuf {
   bool on = false;
   DBuf<int32_t> sn_s, sn_r, col_ptr, col_ids, row_ptr, row_ids, in_ptr, in_idx, out_ptr, out_idx;
   DBuf<int64_t> d_off, m_off, n_off;
-  DBuf<int2> tasks;
+  DBuf<int2> tasks, df_tasks;             // per-level launches / the dataflow order
+  DBuf<int32_t> parent, child_ptr, child_idx, fwd_need, bwd_need, ready;
+  DBuf<unsigned> ticket;
+  int32_t n_fwd_tasks = 0, n_df_tasks = 0, n_sn = 0, df_grid = 0;
+  size_t df_smem = 0;
   std::vector<int32_t> fwd_ptr, bwd_ptr;  // per level: task ranges (forward, backward)
   std::vector<size_t> fwd_smem, bwd_smem;
   DBuf<char> vals, ybuf, cbuf;
   int64_t bytes = 0, n_launch = 0;
   CoarseFactorDev dev() const {
-    return CoarseFactorDev{sn_s.p, sn_r.p, col_ptr.p, col_ids.p, row_ptr.p, row_ids.p,
+    return CoarseFactorDev{parent.p, child_ptr.p, child_idx.p, fwd_need.p, bwd_need.p,
+                           sn_s.p, sn_r.p, col_ptr.p, col_ids.p, row_ptr.p, row_ids.p,
                            d_off.p, m_off.p, n_off.p, in_ptr.p, in_idx.p, out_ptr.p, out_idx.p};
   }
 };
@@ -856,6 +861,15 @@ T* levelset_solve(gdsw_precond* m, const double* r, cudaStream_t s) {
 template <typename T, typename TI>
 void factor_solve(const FactorBuf& F, const TI* u, const int32_t* gmap, T* x, cudaStream_t s) {
   const CoarseFactorDev D = F.dev();
+  static const bool levels = env_flag("GDSW_CF_LEVELS");
+  if (!levels) {
+    // one launch: dependency-driven tiles (k_cf_dataflow)
+    CfSched S{F.ticket.p, F.ready.p, F.ready.p + F.n_sn, F.n_fwd_tasks, F.n_df_tasks, F.n_sn};
+    k_cf_dataflow<T, TI><<<F.df_grid, CF_THREADS, F.df_smem, s>>>(D, S, F.df_tasks.p, (const T*)F.vals.p, u,
+                                                                   gmap, (T*)F.ybuf.p, (T*)F.cbuf.p, x);
+    CK_LAUNCH();
+    return;
+  }
   const int nl = (int)F.fwd_smem.size();
   for (int l = 0; l < nl; ++l) {
     const int32_t t0 = F.fwd_ptr[l], nt = F.fwd_ptr[l + 1] - t0;
@@ -1558,6 +1572,52 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
   for (int l = 0; l < nl; ++l) smax = std::max({smax, F.fwd_smem[l], F.bwd_smem[l]});
   require(smax <= 200 * 1024, "partitioned-inverse supernode too large for shared memory");
   F.tasks.upload(tasks);
+  // dataflow schedule: forward tiles leaves-first, backward tiles root-first;
+  // parent = supernode of the first row below, readiness targets in tiles
+  {
+    std::vector<int32_t> sn_of_col(f->n, -1), par(nsn, -1), nft(nsn), nbt(nsn);
+    for (int k = 0; k < nsn; ++k) {
+      for (int64_t c = f->col_ptr[k]; c < f->col_ptr[k + 1]; ++c) sn_of_col[f->col_ids[c]] = k;
+      nft[k] = (int32_t)((f->sn_s[k] + f->sn_r[k] + CF_ROWS - 1) / CF_ROWS);
+      nbt[k] = (int32_t)((f->sn_s[k] + CF_ROWS - 1) / CF_ROWS);
+    }
+    std::vector<int32_t> cptr(nsn + 1, 0), cidx;
+    for (int k = 0; k < nsn; ++k)
+      if (f->sn_r[k] > 0) {
+        par[k] = sn_of_col[f->row_ids[f->row_ptr[k]]];
+        cptr[par[k] + 1]++;
+      }
+    for (int k = 0; k < nsn; ++k) cptr[k + 1] += cptr[k];
+    cidx.assign(cptr[nsn], 0);
+    std::vector<int32_t> fill(cptr.begin(), cptr.end() - 1), fneed(nsn, 0), bneed(nsn, 0);
+    for (int k = 0; k < nsn; ++k)
+      if (par[k] >= 0) {
+        cidx[fill[par[k]]++] = k;
+        fneed[par[k]] += nft[k];
+      }
+    for (int k = 0; k < nsn; ++k) bneed[k] = nft[k] + (par[k] >= 0 ? nbt[par[k]] : 0);
+    std::vector<int2> df;
+    for (int l = 0; l < nl; ++l)
+      for (int64_t k = f->level_ptr[l]; k < f->level_ptr[l + 1]; ++k)
+        for (int64_t q = 0; q < f->sn_s[k] + f->sn_r[k]; q += CF_ROWS) df.push_back(make_int2((int)k, (int)q));
+    F.n_fwd_tasks = (int32_t)df.size();
+    for (int l = nl - 1; l >= 0; --l)
+      for (int64_t k = f->level_ptr[l]; k < f->level_ptr[l + 1]; ++k)
+        for (int64_t q = 0; q < f->sn_s[k]; q += CF_ROWS) df.push_back(make_int2((int)k, (int)q));
+    F.n_df_tasks = (int32_t)df.size();
+    F.n_sn = nsn;
+    F.df_tasks.upload(df);
+    F.parent.upload(par);
+    F.child_ptr.upload(cptr);
+    F.child_idx.upload(cidx.empty() ? std::vector<int32_t>{0} : cidx);
+    F.fwd_need.upload(fneed);
+    F.bwd_need.upload(bneed);
+    F.ready.alloc(2 * (size_t)std::max(nsn, 1));
+    F.ready.zero();
+    F.ticket.alloc(2);
+    F.ticket.zero();
+    F.df_smem = smax;
+  }
   F.bytes = bytes;
   F.n_launch = 2 * nl;
   with_dtype(dtype, [&](auto tag) {
@@ -1570,7 +1630,13 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
       CK(cudaFuncSetAttribute(k_cf_forward<T, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
       CK(cudaFuncSetAttribute(k_cf_forward<T, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
       CK(cudaFuncSetAttribute(k_cf_backward<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+      CK(cudaFuncSetAttribute(k_cf_dataflow<T, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+      CK(cudaFuncSetAttribute(k_cf_dataflow<T, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
     }
+    // persistent grid: every CTA resident
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cf_dataflow<T, double>, CF_THREADS, smax));
+    F.df_grid = std::max(1, std::min(F.n_df_tasks, num_sms() * std::max(occ, 1)));
   });
   F.on = true;
 }

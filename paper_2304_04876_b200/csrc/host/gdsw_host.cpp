@@ -935,28 +935,38 @@ struct PinvSn {
 };
 
 // dense row-major helpers
+// inverse of a unit lower triangular s x s (strict lower part of a used):
+// row i of the inverse = e_i - sum_{k<i} a[i][k] * (row k of the inverse),
+// rows streamed contiguously
 void tri_inv_unit_lower(i64 s, const std::vector<double>& a, std::vector<double>& inv) {
-  // a: s x s, strictly lower part used (unit diagonal)
   inv.assign((size_t)s * s, 0.0);
-  for (i64 j = 0; j < s; ++j) {
-    inv[j * s + j] = 1.0;
-    for (i64 i = j + 1; i < s; ++i) {
-      double acc = 0.0;
-      for (i64 k = j; k < i; ++k) acc += a[i * s + k] * inv[k * s + j];
-      inv[i * s + j] = -acc;
+  for (i64 i = 0; i < s; ++i) {
+    double* ri = &inv[i * s];
+    for (i64 k = 0; k < i; ++k) {
+      const double f = a[i * s + k];
+      if (f == 0.0) continue;
+      const double* rk = &inv[k * s];
+      for (i64 j = 0; j <= k; ++j) ri[j] -= f * rk[j];
     }
+    ri[i] = 1.0;
   }
 }
 
+// inverse of an upper triangular s x s: row i = (e_i - sum_{k>i} a[i][k] *
+// row k) / a[i][i], from the last row up
 void tri_inv_upper(i64 s, const std::vector<double>& a, std::vector<double>& inv) {
   inv.assign((size_t)s * s, 0.0);
-  for (i64 j = s - 1; j >= 0; --j) {
-    inv[j * s + j] = 1.0 / a[j * s + j];
-    for (i64 i = j - 1; i >= 0; --i) {
-      double acc = 0.0;
-      for (i64 k = i + 1; k <= j; ++k) acc += a[i * s + k] * inv[k * s + j];
-      inv[i * s + j] = -acc / a[i * s + i];
+  for (i64 i = s - 1; i >= 0; --i) {
+    double* ri = &inv[i * s];
+    ri[i] = 1.0;
+    for (i64 k = i + 1; k < s; ++k) {
+      const double f = a[i * s + k];
+      if (f == 0.0) continue;
+      const double* rk = &inv[k * s];
+      for (i64 j = k; j < s; ++j) ri[j] -= f * rk[j];
     }
+    const double d = a[i * s + i];
+    for (i64 j = i; j < s; ++j) ri[j] /= d;
   }
 }
 
