@@ -80,6 +80,19 @@ def parse():
     return p.parse_args()
 
 
+def solver_tuple(token: str):
+    """(method, fill_level, factor_sweeps, trisolve_iters) of a solver token
+    (no product import: the reference arm parses it too)."""
+    name = token.split("(")[0]
+    args = [int(x) for x in token[token.index("(") + 1:-1].split(",")] if "(" in token else []
+    if name == "exact_lu":
+        return ("exact_lu", 0, 3, 5)
+    if name == "ilu_k":
+        return ("ilu_k", (args[:1] or [0])[0], 3, 5)
+    fill, sweeps, iters = (args + [0, 3, 5][len(args):])[:3]
+    return ("fast_ilu", fill, sweeps, iters)
+
+
 def solver_spec(token: str):
     from paper_2304_04876_b200.local_solvers import SolverSpec
     name = token.split("(")[0]
@@ -459,6 +472,15 @@ def cpu_baseline(args, prob, dec, cfg, skel, pre, b, iterations):
                       "oracle FastILU factors, coarse basis from the GPU setup"}
 
 
+def _loaded_libraries() -> list:
+    """Shared objects mapped into this process (/proc/self/maps)."""
+    try:
+        return sorted({line.split()[-1] for line in open("/proc/self/maps")
+                       if line.rstrip().endswith(".so") and "/repo" in line})
+    except OSError:
+        return []
+
+
 def cpu_model() -> str:
     """`lscpu`'s model name (BASELINE.md section 2 asks for it)."""
     try:
@@ -487,9 +509,21 @@ def reference(args):
         threadpool_limits(cores)
     except Exception:
         pass
-    prob, dec, cfg = build_problem(args)
+    method, fill, sweeps, iters = solver_tuple(args.solver)
     t0 = time.perf_counter()
-    ore = O.OracleSchwarz(prob.a, dec, cfg, prob.nullspace, threads=cores)
+    if (method == "fast_ilu" and fill == 0 and args.ordering == "natural"
+            and args.precision == "double"):
+        # the reference's setup restated inside the oracle (numpy + scipy +
+        # liboracle): nothing of the product is loaded on this arm
+        from oracle.reference_setup import IndependentSchwarz
+        ore = IndependentSchwarz(args.n, args.n, args.n, args.parts, args.parts, args.parts,
+                                 sweeps, iters, threads=cores)
+        prob = types.SimpleNamespace(a=ore.a)
+        setup_kind = "oracle/reference_setup.py (independent of the product)"
+    else:
+        prob, dec, cfg = build_problem(args)
+        ore = O.OracleSchwarz(prob.a, dec, cfg, prob.nullspace, threads=cores)
+        setup_kind = "product host layer for index sets (configuration outside reference_setup)"
     t_setup = time.perf_counter() - t0
     x_star = np.random.default_rng(0).standard_normal(prob.a.nrows)
     b = prob.a @ x_star
@@ -511,7 +545,8 @@ def reference(args):
               f"system from x0 = 0 to rtol 1e-7 ({iters} iterations, true relative residual "
               f"{true_rel:.2e}), subdomain solves on {cores} threads (the reference's `threads` "
               f"option) and BLAS on {cores} threads; {args.warmup} warm-up samples of "
-              f"{args.cpu_sample_iters} iterations; setup {t_setup:.1f}s not timed")
+              f"{args.cpu_sample_iters} iterations; setup {t_setup:.1f}s not timed, built by "
+              f"{setup_kind}")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "s", "n_gpus": world,
         "steps": len(times), "steps_requested": args.steps, "warmup": args.warmup,
@@ -522,6 +557,7 @@ def reference(args):
         "true_relative_residual": true_rel,
         "cpu_baseline": {"value": value, "unit": "s", "cores": cores, "kind": "port",
                          "cpu_model": cpu_model(), "sample": sample},
+        "loaded_native": sorted({Path(p).name for p in _loaded_libraries()}),
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 

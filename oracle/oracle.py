@@ -132,6 +132,8 @@ def _norm_inf(ptr, vals) -> float:
 
 
 def _permuted(block, perm):
+    if np.array_equal(perm, np.arange(len(perm))):
+        return block    # natural ordering (reference_setup: no product import)
     from paper_2304_04876_b200.sparse_core import permute_symmetric
     return permute_symmetric(block, perm)
 

@@ -170,7 +170,9 @@ __global__ void __launch_bounds__(CF_THREADS) k_cf_dataflow(CoarseFactorDev F, C
     if (t >= S.n_tasks) break;
     const bool fwd = t < S.n_fwd;
     const int2 tk = tasks[t];
-    const int k = tk.x, row0 = tk.y;
+    // tile: rows [row0, row0 + nrows) of the stacked block (sized per level
+    // at install: enough tiles to fill the GPU, no more)
+    const int k = tk.x, row0 = tk.y & 0xFFFF, nrows = tk.y >> 16;
     const int s = F.sn_s[k], r = F.sn_r[k];
     const int32_t* cols = F.col_ids + F.col_ptr[k];
     if (threadIdx.x == 0) {
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(CF_THREADS) k_cf_dataflow(CoarseFactorDev F, C
         buf[i] = acc;
       }
       __syncthreads();
-      for (int q = warp; q < CF_ROWS; q += CF_THREADS / 32) {
+      for (int q = warp; q < nrows; q += CF_THREADS / 32) {
         const int row = row0 + q;
         if (row >= s + r) break;
         if (row < s) {
@@ -208,7 +210,7 @@ __global__ void __launch_bounds__(CF_THREADS) k_cf_dataflow(CoarseFactorDev F, C
       for (int i = threadIdx.x; i < s + r; i += CF_THREADS)
         buf[i] = i < s ? __ldcg(y + cols[i]) : __ldcg(x + rows[i - s]);
       __syncthreads();
-      for (int q = warp; q < CF_ROWS; q += CF_THREADS / 32) {
+      for (int q = warp; q < nrows; q += CF_THREADS / 32) {
         const int row = row0 + q;
         if (row >= s) break;
         const T a = cf_dot(vals + F.d_off[k] + (int64_t)row * s, buf, row, s, lane);

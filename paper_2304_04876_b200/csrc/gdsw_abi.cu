@@ -1572,14 +1572,51 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
   for (int l = 0; l < nl; ++l) smax = std::max({smax, F.fwd_smem[l], F.bwd_smem[l]});
   require(smax <= 200 * 1024, "partitioned-inverse supernode too large for shared memory");
   F.tasks.upload(tasks);
+  if (smax > 48 * 1024) {  // before the occupancy query below
+    auto big = [&](auto kern) { CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax)); };
+    big(k_cf_forward<double, double>);
+    big(k_cf_forward<float, double>);
+    big(k_cf_forward<float, float>);
+    big(k_cf_backward<double>);
+    big(k_cf_backward<float>);
+    big(k_cf_dataflow<double, double>);
+    big(k_cf_dataflow<float, double>);
+    big(k_cf_dataflow<float, float>);
+  }
   // dataflow schedule: forward tiles leaves-first, backward tiles root-first;
-  // parent = supernode of the first row below, readiness targets in tiles
+  // parent = supernode of the first row below, readiness targets in tiles.
+  // Tile rows per level and direction: about two tiles per resident CTA
+  // slot (C3's 512 blocks: large tiles, few per-task overheads; a coarse
+  // level of one supernode: 8-row tiles over the whole GPU)
   {
-    std::vector<int32_t> sn_of_col(f->n, -1), par(nsn, -1), nft(nsn), nbt(nsn);
+    int occ = 0;
+    if (dtype == GDSW_F32)
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cf_dataflow<float, double>, CF_THREADS, smax));
+    else
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cf_dataflow<double, double>, CF_THREADS, smax));
+    const int64_t slots = (int64_t)num_sms() * std::max(occ, 1);
+    std::vector<int32_t> tile_f(nl), tile_b(nl);
+    for (int l = 0; l < nl; ++l) {
+      int64_t rf = 0, rb = 0;
+      for (int64_t k = f->level_ptr[l]; k < f->level_ptr[l + 1]; ++k) {
+        rf += f->sn_s[k] + f->sn_r[k];
+        rb += f->sn_s[k];
+      }
+      auto pick = [&](int64_t rows) {
+        int64_t t = (rows + 2 * slots - 1) / (2 * slots);
+        t = std::min<int64_t>(128, std::max<int64_t>(CF_ROWS, (t + 7) / 8 * 8));
+        return (int32_t)t;
+      };
+      tile_f[l] = pick(rf);
+      tile_b[l] = pick(rb);
+    }
+    std::vector<int32_t> sn_of_col(f->n, -1), par(nsn, -1), nft(nsn), nbt(nsn), lev(nsn);
+    for (int l = 0; l < nl; ++l)
+      for (int64_t k = f->level_ptr[l]; k < f->level_ptr[l + 1]; ++k) lev[k] = l;
     for (int k = 0; k < nsn; ++k) {
       for (int64_t c = f->col_ptr[k]; c < f->col_ptr[k + 1]; ++c) sn_of_col[f->col_ids[c]] = k;
-      nft[k] = (int32_t)((f->sn_s[k] + f->sn_r[k] + CF_ROWS - 1) / CF_ROWS);
-      nbt[k] = (int32_t)((f->sn_s[k] + CF_ROWS - 1) / CF_ROWS);
+      nft[k] = (int32_t)((f->sn_s[k] + f->sn_r[k] + tile_f[lev[k]] - 1) / tile_f[lev[k]]);
+      nbt[k] = (int32_t)((f->sn_s[k] + tile_b[lev[k]] - 1) / tile_b[lev[k]]);
     }
     std::vector<int32_t> cptr(nsn + 1, 0), cidx;
     for (int k = 0; k < nsn; ++k)
@@ -1597,13 +1634,18 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
       }
     for (int k = 0; k < nsn; ++k) bneed[k] = nft[k] + (par[k] >= 0 ? nbt[par[k]] : 0);
     std::vector<int2> df;
+    auto tile = [](int64_t k, int64_t q, int64_t rows, int64_t t) {
+      require(q < 65536, "partitioned-inverse supernode too tall for the tile encoding");
+      return make_int2((int)k, (int)(q | (std::min<int64_t>(t, rows - q) << 16)));
+    };
     for (int l = 0; l < nl; ++l)
       for (int64_t k = f->level_ptr[l]; k < f->level_ptr[l + 1]; ++k)
-        for (int64_t q = 0; q < f->sn_s[k] + f->sn_r[k]; q += CF_ROWS) df.push_back(make_int2((int)k, (int)q));
+        for (int64_t q = 0; q < f->sn_s[k] + f->sn_r[k]; q += tile_f[l])
+          df.push_back(tile(k, q, f->sn_s[k] + f->sn_r[k], tile_f[l]));
     F.n_fwd_tasks = (int32_t)df.size();
     for (int l = nl - 1; l >= 0; --l)
       for (int64_t k = f->level_ptr[l]; k < f->level_ptr[l + 1]; ++k)
-        for (int64_t q = 0; q < f->sn_s[k]; q += CF_ROWS) df.push_back(make_int2((int)k, (int)q));
+        for (int64_t q = 0; q < f->sn_s[k]; q += tile_b[l]) df.push_back(tile(k, q, f->sn_s[k], tile_b[l]));
     F.n_df_tasks = (int32_t)df.size();
     F.n_sn = nsn;
     F.df_tasks.upload(df);
@@ -1626,13 +1668,6 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
     upload_cast<T>(F.vals, h);
     F.ybuf.alloc((size_t)f->n * sizeof(T));
     F.cbuf.alloc((size_t)std::max<int64_t>(nrow, 1) * sizeof(T));
-    if (smax > 48 * 1024) {
-      CK(cudaFuncSetAttribute(k_cf_forward<T, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
-      CK(cudaFuncSetAttribute(k_cf_forward<T, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
-      CK(cudaFuncSetAttribute(k_cf_backward<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
-      CK(cudaFuncSetAttribute(k_cf_dataflow<T, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
-      CK(cudaFuncSetAttribute(k_cf_dataflow<T, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
-    }
     // persistent grid: every CTA resident
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cf_dataflow<T, double>, CF_THREADS, smax));

@@ -126,7 +126,7 @@ class DistPreconditioner:
         import torch.distributed as tdist
 
         from . import device
-        from .schwarz import _gpu_lu_pays
+        from .schwarz import _gpu_lu_pays, _install_local_factor, _local_factor_pays
         self.shard = sh = shard
         spec = config.local
         single = config.precision == "single"
@@ -181,6 +181,8 @@ class DistPreconditioner:
                 lvs.append(lv)
                 uvs.append(uv)
             self.pre.set_factors(np.concatenate(lvs).astype(vdt), np.concatenate(uvs).astype(vdt))
+        if spec.method == "exact_lu" and _local_factor_pays(syms):
+            _install_local_factor(self.pre, self.plan, syms)
         self.coarse_n = 0
         if config.use_coarse:
             self._coarse(a, coarse_src, a_ext, a_ext_dev, dec, nullspace, config, single,

@@ -484,8 +484,8 @@ def setup_numeric(skeleton: PreconditionerSkeleton, a: CsrMatrix,
         pre.set_factors(_cat(lvs, value_dtype), _cat(uvs, value_dtype))
 
     tick("local factors")
-    if spec.method == "exact_lu" and _local_factor_pays(skeleton):
-        _install_local_factor(pre, plan, skeleton)
+    if spec.method == "exact_lu" and _local_factor_pays(skeleton.local_symbolics):
+        _install_local_factor(pre, plan, skeleton.local_symbolics)
         tick("local partitioned inverses")
     coarse = None
     if config.use_coarse:
@@ -530,7 +530,7 @@ def _coarse_lu_thunk(a0, ordering):
     return lambda: numeric_lu(a0, symbolic_lu(a0, make_ordering(a0, ordering)))
 
 
-def _local_factor_pays(skeleton) -> bool:
+def _local_factor_pays(syms) -> bool:
     """Exact-LU blocks solve through supernodal partitioned inverses
     (coarse_factor.build_block_factors): the nested-dissection elimination
     tree's height (C1: 12 levels) replaces the level schedule's one-row
@@ -539,14 +539,12 @@ def _local_factor_pays(skeleton) -> bool:
     force = os.environ.get("GDSW_LOCAL_FACTOR", "")
     if force in ("0", "1"):
         return force == "1"
-    syms = skeleton.local_symbolics
     fill = sum(s.l_idx.size + s.u_idx.size for s in syms)
     return fill <= 2_000_000_000 and max(s.n for s in syms) <= 20_000
 
 
-def _install_local_factor(pre, plan, skeleton):
+def _install_local_factor(pre, plan, syms):
     from .coarse_factor import build_block_factors
-    syms = skeleton.local_symbolics
     lv, uv = pre.factors(plan.nnz_l, plan.nnz_u)
     blocks, base, lo, uo = [], 0, 0, 0
     for sym in syms:

@@ -119,3 +119,50 @@ def test_oracle_kernels_on_dense_oracles():
     assert np.array_equal(y, a @ x)
     blk = extract_submatrix(a, np.arange(10), np.arange(10))
     assert blk.nrows == 10
+
+
+# ---------------------------------------------------------------------------
+# the reference arm's own setup (oracle/reference_setup.py): pinned against
+# the reference's decomposition hashes and apply, independent of the product
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name,n,p", [("lap64_fast_p4", 64, 4), ("lap64_fast_p8", 64, 8)])
+def test_reference_setup_decomposition_matches_reference(golden_dir, name, n, p):
+    import json
+
+    from oracle import reference_setup as R
+    want = json.loads((golden_dir / "configs" / f"{name}.json").read_text())
+    a, _ = R.assemble_laplace3d(n, n, n)
+    owner = R.box_partition(n, n, n, p, p, p)
+    sets = R.extend_overlap(a, owner, p ** 3, 1)
+    st = R.build_rgdsw(R.classify_interface(a, owner))
+    assert R.decomposition_hash(sets, st) == want["dec_hash"]
+    assert len(st.components) == want["n_coarse"]
+
+
+def test_reference_setup_apply_and_solve_match_reference(golden_dir):
+    """64^3, 4x4x4, fast_ilu(0,3,5): the independently built preconditioner
+    applies like the reference (1e-10) and GMRES takes its iteration count;
+    the build loads nothing of the product."""
+    import json
+    import subprocess
+    import sys
+    code = (
+        "import sys, json, numpy as np\n"
+        f"sys.path.insert(0, {str(golden_dir.parents[1])!r})\n"
+        "from oracle import reference_setup as R\n"
+        "from oracle import oracle as O\n"
+        "S = R.IndependentSchwarz(64, 64, 64, 4, 4, 4, threads=4)\n"
+        "r = np.random.default_rng(1).standard_normal(64 ** 3)\n"
+        f"zr = np.load({str(golden_dir / 'configs' / 'lap64_fast_p4.npz')!r})['apply_probe1']\n"
+        "rel = float(np.abs(S.apply(r) - zr).max() / np.abs(zr).max())\n"
+        "b = S.a @ np.random.default_rng(0).standard_normal(64 ** 3)\n"
+        "_, rep = O.gmres(lambda v: O.csr_spmv(S.a, v), S.apply, b)\n"
+        "mods = sorted(m for m in sys.modules if m.startswith('paper_2304'))\n"
+        "print(json.dumps(dict(rel=rel, its=rep['iterations'], mods=mods)))\n")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         timeout=600, check=True).stdout
+    got = json.loads(out.strip().splitlines()[-1])
+    want = json.loads((golden_dir / "configs" / "lap64_fast_p4.json").read_text())
+    assert got["rel"] <= 1e-10
+    assert got["its"] == want["iterations"]
+    assert got["mods"] == []
