@@ -48,7 +48,8 @@ struct CoarseFactorDev {
 // dot of a dense row segment [j0, j1) with a shared-memory vector: lanes
 // over the columns, eight independent partial sums (eight row loads in
 // flight per lane: one row per warp must keep HBM busy on its own when a
-// level holds few supernodes)
+// level holds few supernodes). Measured: a predicated tail (all of a short
+// row's loads at once) and eight rows per warp were both slower.
 template <typename T>
 __device__ __forceinline__ T cf_dot(const T* __restrict__ row, const T* vec, int j0, int j1, int lane) {
   T a[8];

@@ -835,13 +835,16 @@ T* levelset_solve(gdsw_precond* m, const double* r, cudaStream_t s) {
                        : (need <= 110 * 1024 ? 110 * 1024 : (need <= 220 * 1024 ? 220 * 1024 : 160 * 1024));
   if (ring_env) budget = ring_env;
   const bool smx = budget - xs >= min_chunks * ts.chunk_max && !env_flag("GDSW_TS_XGLOBAL");
-  const int64_t ring = std::max<int64_t>(2LL * ts.chunk_max, ((smx ? budget - xs : budget) & ~int64_t(15)));
+  int64_t ring = std::max<int64_t>(2LL * ts.chunk_max, ((smx ? budget - xs : budget) & ~int64_t(15)));
+  // forwarding + PSV buffers (4 x TR_FWD static values) when the iterate
+  // stays in global memory
+  if (!smx && ts.fwd) ring = std::min<int64_t>(ring, (220 * 1024 - 4 * TR_FWD * (int64_t)sizeof(T)) & ~int64_t(15));
   const size_t smem = (size_t)ring + (smx ? (size_t)xs : 0);
   require(smem <= 220 * 1024, "streamed SpTRSV chunk too large");
   // forwarding slots: only with the iterate in global memory; the static
   // forwarding buffers (2 x TR_FWD values) come out of the budget
   const bool fwd = ts.fwd && !smx;
-  if (fwd) require(smem + 2 * TR_FWD * sizeof(T) <= 220 * 1024 && smem <= 200 * 1024,
+  if (fwd) require(smem + 4 * TR_FWD * sizeof(T) <= 220 * 1024 && ring >= 2LL * ts.chunk_max,
                    "streamed SpTRSV chunk too large");
   if (ts.csize == 2) {
     if (smx) launch_stream<T, uint16_t, true>(m, r, y, (int32_t)ring, smem, s);
@@ -1602,8 +1605,12 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
         rf += f->sn_s[k] + f->sn_r[k];
         rb += f->sn_s[k];
       }
+      static const int64_t tps = [] {
+        const char* e = std::getenv("GDSW_CF_TPS");
+        return e ? std::max<int64_t>(1, std::atoi(e)) : (int64_t)2;
+      }();
       auto pick = [&](int64_t rows) {
-        int64_t t = (rows + 2 * slots - 1) / (2 * slots);
+        int64_t t = (rows + tps * slots - 1) / (tps * slots);
         t = std::min<int64_t>(128, std::max<int64_t>(CF_ROWS, (t + 7) / 8 * 8));
         return (int32_t)t;
       };
