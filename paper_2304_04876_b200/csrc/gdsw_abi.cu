@@ -774,8 +774,13 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
 template <typename T, typename CT, bool SMEMX, bool FWD, int NW>
 void launch_stream_nw(gdsw_precond* m, const double* r, T* y, int32_t ring, size_t smem, cudaStream_t s) {
   static bool attr = [] {
+    // dynamic shared memory up to the 227 KB opt-in limit minus the
+    // kernel's static buffers (forwarding: 16 KB in fp64)
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, k_trisolve_stream<T, CT, SMEMX, FWD, NW>));
+    const int cap = std::min<int>(220 * 1024, 227 * 1024 - (int)fa.sharedSizeBytes);
     CK(cudaFuncSetAttribute(k_trisolve_stream<T, CT, SMEMX, FWD, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            FWD ? 200 * 1024 : 220 * 1024));
+                            cap));
     return true;
   }();
   (void)attr;
@@ -836,15 +841,15 @@ T* levelset_solve(gdsw_precond* m, const double* r, cudaStream_t s) {
   if (ring_env) budget = ring_env;
   const bool smx = budget - xs >= min_chunks * ts.chunk_max && !env_flag("GDSW_TS_XGLOBAL");
   int64_t ring = std::max<int64_t>(2LL * ts.chunk_max, ((smx ? budget - xs : budget) & ~int64_t(15)));
-  // forwarding + PSV buffers (4 x TR_FWD static values) when the iterate
-  // stays in global memory
-  if (!smx && ts.fwd) ring = std::min<int64_t>(ring, (220 * 1024 - 4 * TR_FWD * (int64_t)sizeof(T)) & ~int64_t(15));
+  // forwarding buffers (2 x TR_FWD static values) when the iterate stays in
+  // global memory
+  if (!smx && ts.fwd) ring = std::min<int64_t>(ring, (220 * 1024 - 2 * TR_FWD * (int64_t)sizeof(T)) & ~int64_t(15));
   const size_t smem = (size_t)ring + (smx ? (size_t)xs : 0);
   require(smem <= 220 * 1024, "streamed SpTRSV chunk too large");
   // forwarding slots: only with the iterate in global memory; the static
   // forwarding buffers (2 x TR_FWD values) come out of the budget
   const bool fwd = ts.fwd && !smx;
-  if (fwd) require(smem + 4 * TR_FWD * sizeof(T) <= 220 * 1024 && ring >= 2LL * ts.chunk_max,
+  if (fwd) require(smem + 2 * TR_FWD * sizeof(T) <= 220 * 1024 && ring >= 2LL * ts.chunk_max,
                    "streamed SpTRSV chunk too large");
   if (ts.csize == 2) {
     if (smx) launch_stream<T, uint16_t, true>(m, r, y, (int32_t)ring, smem, s);

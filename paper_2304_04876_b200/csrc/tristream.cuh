@@ -71,9 +71,7 @@ struct TriStreamDev {
   const int32_t* ch_sub = nullptr;   // [n_sub + 1] chunk range of each subdomain (L chunks, then U)
   const int64_t* ch_off = nullptr;   // byte offset of each chunk
   const int32_t* ch_len = nullptr;   // bytes of each chunk (multiple of 16)
-  const int32_t* ch_lsplit = nullptr;  // [n_sub] first U chunk of each subdomain
   int32_t chunk_max = 0;
-  int32_t psv = 0;  // the producer stages the short rows' starting values
 };
 
 // ---------------------------------------------------------------------------
@@ -84,9 +82,8 @@ struct TriStream {
   int32_t chunk_max = 0;
   int vsize = 8, csize = 4;
   bool fwd = false;  // slices carry forwarding slots (iterate too large for shared memory)
-  bool has_sn = false;  // supernodal chunks present (they update later rows' starting values)
   DBuf<unsigned char> bytes;
-  DBuf<int32_t> ch_sub, ch_len, ch_lsplit;
+  DBuf<int32_t> ch_sub, ch_len;
   DBuf<int64_t> ch_off;
   // value placement: element (vsize) offsets into the stream
   DBuf<int64_t> pl_src, pl_dst;
@@ -140,8 +137,7 @@ struct TriStream {
     std::vector<int32_t> ch_of, slot_of;  // chunk / slot of each short row of the current pass
 
     std::vector<unsigned char> buf;
-    std::vector<int32_t> h_ch_sub(n_sub + 1), h_ch_len, h_ch_lsplit(n_sub);
-    has_sn = false;
+    std::vector<int32_t> h_ch_sub(n_sub + 1), h_ch_len;
     std::vector<int64_t> h_ch_off, p_src, p_dst;
     std::vector<int32_t> p_len, p_stride;
 
@@ -376,7 +372,6 @@ struct TriStream {
       const int64_t base = sub_ptr[s];
       for (const Fac* f : {&L, &U}) {
         up = f->skip == 1;
-        if (up) h_ch_lsplit[s] = (int32_t)h_ch_off.size();
         const std::vector<int64_t>& ptr = *f->ptr;
         const int64_t n_s = sub_ptr[s + 1] - base;
         const std::vector<int64_t>& idx = *f->idx;
@@ -415,7 +410,6 @@ struct TriStream {
               while (j < n_s && nests(j - 1, j)) ++j;
             }
             if (!bitwise && j - i >= TR_SN_MIN) {
-              has_sn = true;
               SN sn{i, j - i, up ? rlen(j - 1) : rlen(i)};
               for (int64_t r = i; r < j; ++r) sn_of[r] = (int32_t)sns.size();
               sns.push_back(sn);
@@ -507,7 +501,6 @@ struct TriStream {
     n_chunks = (int64_t)h_ch_off.size();
     bytes.upload(buf.data(), std::max<size_t>(buf.size(), 16));
     ch_sub.upload(h_ch_sub);
-    ch_lsplit.upload(h_ch_lsplit);
     ch_off.upload(h_ch_off);
     ch_len.upload(h_ch_len);
     pl_src.upload(p_src);
@@ -522,13 +515,7 @@ struct TriStream {
     v.ch_sub = ch_sub.p;
     v.ch_off = ch_off.p;
     v.ch_len = ch_len.p;
-    v.ch_lsplit = ch_lsplit.p;
     v.chunk_max = chunk_max;
-    static const bool psv_off = [] {
-      const char* e = std::getenv("GDSW_TS_PSV");
-      return e && e[0] == '0';
-    }();
-    v.psv = fwd && !has_sn && !psv_off;
     return v;
   }
 };
@@ -649,7 +636,7 @@ __device__ __forceinline__ void ts_sn_chunk(const unsigned char* __restrict__ c,
 
 template <typename T, typename CT, bool FWD, int NW>
 __device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T* x, T* part, const T* fprev,
-                                         T* fcur, const T* sval) {
+                                         T* fcur) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int4 hdr = *reinterpret_cast<const int4*>(c);
   if (hdr.w != TR_ROWS) {
@@ -716,9 +703,7 @@ __device__ __forceinline__ void ts_chunk(const unsigned char* __restrict__ c, T*
     const T* v = reinterpret_cast<const T*>(c + st.x) + (t & 31);
     const CT* cc = reinterpret_cast<const CT*>(c + st.y) + (t & 31);
     const uint16_t* fs = FWD ? reinterpret_cast<const uint16_t*>(c + st.w) + (t & 31) : nullptr;
-    // starting value: staged in shared memory by the producer warp (PSV),
-    // else the iterate (an L2 round trip on the level's critical path)
-    T acc = (FWD && sval != nullptr && t < TR_FWD) ? sval[t] : x[row];
+    T acc = x[row];
     for (int k0 = 0; k0 < len; k0 += 4) {
       T pv[4], xv[4];
 #pragma unroll
@@ -774,8 +759,6 @@ __global__ void __launch_bounds__(32 * NW + 32) k_trisolve_stream(TriStreamDev S
   __shared__ int32_t pos[TR_NT], foot[TR_NT];
   __shared__ T part[TR_MAXW];
   __shared__ T fwdbuf[FWD ? 2 * TR_FWD : 1];
-  __shared__ T sval[FWD ? 2 * TR_FWD : 1];   // PSV: staged starting values, double buffered
-  __shared__ uint64_t svb[2];
   const int s = blockIdx.x;
   const int32_t base = sub_ptr[s], ns = sub_ptr[s + 1] - base;
   const int c0 = S.ch_sub[s], c1 = S.ch_sub[s + 1];
@@ -787,46 +770,13 @@ __global__ void __launch_bounds__(32 * NW + 32) k_trisolve_stream(TriStreamDev S
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(&svb[0], 1);
-    mbar_init(&svb[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const bool psv = FWD && S.psv;
-  const int nch_l = S.ch_lsplit[s] - c0;
   if (threadIdx.x >= (32 * NW)) {
     // producer warp: the chunk table is read 32 entries at a time, one
-    // window ahead; lane 0 issues the copies. With PSV it also stages each
-    // chunk's short-row starting values into sval (a landed chunk's row
-    // table; L: the gathered residual, U: the L solution) two chunks behind
-    // the copies, so a level never waits on an L2 load of its own rows.
+    // window ahead; lane 0 issues the copies
     const int lane = threadIdx.x & 31;
-    int pf = 0;
-    auto stage_upto = [&](int last) {
-      for (; pf <= last; ++pf) {
-        const int j = pf, t = j % TR_NT;
-        mbar_wait(&full[t], (uint32_t)((j / TR_NT) & 1));
-        if (j >= 2) mbar_wait(&empty[(j - 2) % TR_NT], (uint32_t)(((j - 2) / TR_NT) & 1));
-        const bool upper = j >= nch_l;
-        if (upper && j >= 1) mbar_wait(&empty[(j - 1) % TR_NT], (uint32_t)(((j - 1) / TR_NT) & 1));
-        const unsigned char* c = ring + pos[t];
-        const int4 hdr = *reinterpret_cast<const int4*>(c);
-        T* sv = sval + (j & 1) * TR_FWD;
-        if (hdr.w == TR_ROWS) {
-          const ChunkLayout cl(hdr.x, hdr.y, hdr.z & 1, (int)sizeof(T));
-          const int32_t* srow = reinterpret_cast<const int32_t*>(c + cl.srow);
-          const int32_t* slen = reinterpret_cast<const int32_t*>(c + cl.slen);
-          const int nt = min(32 * hdr.y, TR_FWD);
-          for (int q = lane; q < nt; q += 32) {
-            if (slen[q] < 0) continue;
-            const int32_t row = srow[q];
-            sv[q] = upper ? x[row] : (T)r[gmap[base + row]];
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&svb[j & 1]);
-      }
-    };
     int64_t off_c = 0, off_n = 0;
     int32_t len_c = 0, len_n = 0;
     if (lane < nch) {
@@ -845,31 +795,25 @@ __global__ void __launch_bounds__(32 * NW + 32) k_trisolve_stream(TriStreamDev S
       }
       const int64_t off = __shfl_sync(0xffffffffu, off_c, i & 31);
       const int32_t len = __shfl_sync(0xffffffffu, len_c, i & 31);
-      // every lane keeps the same ring bookkeeping; lane 0 issues
-      const int t = i % TR_NT;
-      const int start = head + len <= ring_bytes ? head : 0;
-      const int fp = len + (start == 0 && head != 0 ? ring_bytes - head : 0);
-      // retire consumed chunks until the ticket and the bytes are free (the
-      // consumers of a chunk need its staged starting values first)
-      while (oldest < i && (i - oldest >= TR_NT || inflight + fp > ring_bytes)) {
-        if (psv) stage_upto(oldest);
-        mbar_wait(&empty[oldest % TR_NT], (uint32_t)((oldest / TR_NT) & 1));
-        inflight -= foot[oldest % TR_NT];
-        ++oldest;
-      }
-      __syncwarp();
       if (lane == 0) {
+        const int t = i % TR_NT;
+        const int start = head + len <= ring_bytes ? head : 0;
+        const int fp = len + (start == 0 && head != 0 ? ring_bytes - head : 0);
+        // retire consumed chunks until the ticket and the bytes are free
+        while (oldest < i && (i - oldest >= TR_NT || inflight + fp > ring_bytes)) {
+          mbar_wait(&empty[oldest % TR_NT], (uint32_t)((oldest / TR_NT) & 1));
+          inflight -= foot[oldest % TR_NT];
+          ++oldest;
+        }
         pos[t] = start;
         foot[t] = fp;
+        inflight += fp;
+        head = start + len;
         mbar_expect_tx(&full[t], (uint32_t)len);
         bulk_g2s(ring + start, S.bytes + off, (uint32_t)len, &full[t]);
       }
-      inflight += fp;
-      head = start + len;
       __syncwarp();
-      if (psv && i >= 2) stage_upto(i - 2);
     }
-    if (psv) stage_upto(nch - 1);
     return;
   }
   for (int32_t k = threadIdx.x; k < ns; k += (32 * NW)) x[k] = (T)r[gmap[base + k]];
@@ -877,10 +821,8 @@ __global__ void __launch_bounds__(32 * NW + 32) k_trisolve_stream(TriStreamDev S
   for (int i = 0; i < nch; ++i) {
     const int t = i % TR_NT;
     mbar_wait(&full[t], (uint32_t)((i / TR_NT) & 1));
-    if (psv) mbar_wait(&svb[i & 1], (uint32_t)((i >> 1) & 1));
     ts_chunk<T, CT, FWD, NW>(ring + pos[t], x, part, fwdbuf + ((i & 1) ^ 1) * (FWD ? TR_FWD : 0),
-                             fwdbuf + (i & 1) * (FWD ? TR_FWD : 0),
-                             psv ? sval + (i & 1) * TR_FWD : nullptr);
+                         fwdbuf + (i & 1) * (FWD ? TR_FWD : 0));
     consumer_bar<NW>();
     if (threadIdx.x == 0) mbar_arrive(&empty[t]);
   }
