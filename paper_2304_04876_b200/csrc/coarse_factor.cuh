@@ -198,12 +198,17 @@ __global__ void __launch_bounds__(CF_THREADS) k_cf_dataflow(CoarseFactorDev F, C
           const T acc = cf_dot(vals + F.d_off[k] + (int64_t)row * s, buf, 0, row, lane);
           if (lane == 0) y[cols[row]] = acc + buf[row];
         } else {
+          // the children's updates on this row (extend-add) are loaded by
+          // the lanes before the dot, so their latency overlaps its loads;
+          // added in list order after it
+          const int32_t g = F.row_ptr[k] + row - s;
+          const int32_t p0 = F.out_ptr[g], np = F.out_ptr[g + 1] - p0;
+          T extra = T(0);
+          if (lane < np) extra = __ldcg(cbuf + F.out_idx[p0 + lane]);
           T acc = cf_dot(vals + F.m_off[k] + (int64_t)(row - s) * s, buf, 0, s, lane);
-          if (lane == 0) {
-            const int32_t g = F.row_ptr[k] + row - s;
-            for (int32_t p = F.out_ptr[g]; p < F.out_ptr[g + 1]; ++p) acc += __ldcg(cbuf + F.out_idx[p]);
-            cbuf[g] = acc;
-          }
+          for (int e = 0; e < min(np, 32); ++e) acc += __shfl_sync(0xffffffffu, extra, e);
+          for (int32_t p = p0 + 32; p < p0 + np; ++p) acc += __ldcg(cbuf + F.out_idx[p]);
+          if (lane == 0) cbuf[g] = acc;
         }
       }
     } else {

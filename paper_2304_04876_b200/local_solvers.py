@@ -8,11 +8,16 @@ phase and solves on the GPU (mirrors schwarzdd.local_solvers).
   triangular solves, and the same sha256 `structure_hash`.
 * Numeric: `fast_ilu` runs its fixed-point sweeps on the GPU (batched over
   subdomains, see schwarz.setup_numeric / device.Precond.fastilu);
-  `exact_lu` and `ilu_k` use the pattern-restricted IKJ kernel on the host
-  (local_solvers.py:306-340) -- GPU numeric LU is the next row of the build.
-* Solves (`LocalFactorization.solve`, `trisolve_levelset`, `fast_trisolve`)
-  run on the GPU through a one-subdomain context: level-set SpTRSV for
-  exact/ILU factors, Jacobi FastSpTRSV for fast_ilu factors.
+  `exact_lu` and `ilu_k` run the reference's pattern-restricted IKJ kernel
+  (local_solvers.py:306-340) on the GPU, every block in one launch and
+  bit-identical to the host kernel; separator-heavy exact factors with few
+  blocks keep the parallel host kernel (schwarz._gpu_lu_pays).
+* Solves: inside the preconditioner every block is solved in one launch --
+  Jacobi FastSpTRSV for fast_ilu, the TMA-streamed level-set SpTRSV for
+  ILU(k), supernodal partitioned inverses for exact factors (coarse_factor.py)
+  when the blocks fit twice over the SMs. `LocalFactorization.solve`
+  (`trisolve_levelset`, `fast_trisolve`) runs the same kernels through a
+  one-subdomain context.
 
 L has a unit diagonal (not stored); U stores its diagonal first per row.
 """
