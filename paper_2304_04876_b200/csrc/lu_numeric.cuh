@@ -3,7 +3,9 @@
 // local_solvers.py:306-340; host restatement gdsw_host.cpp lu_numeric).
 //
 // One CTA per subdomain walks the L level schedule (row i needs the U rows
-// k in L(i), all in earlier levels); each warp factors one row of a level:
+// k in L(i), all in earlier levels); each warp factors one row of a level
+// (levels of at most LU_COOP_ROWS rows -- separator chains -- use the whole
+// CTA per row, the j updates of each k over all threads):
 //   w[pattern(i)] = 0; w[j] = a_ij (+ shift on the diagonal) for j in A(i)
 //   for k in L(i) ascending:  l = w[k] / u_kk;  w[k] = l;
 //                             w[j] -= l * u_kj  for j in U(k) \ {k}, j in pattern(i)
@@ -19,6 +21,7 @@ namespace gdsw {
 
 constexpr int LU_WARPS = 8;
 constexpr int LU_THREADS = 32 * LU_WARPS;
+constexpr int LU_COOP_ROWS = 2;  // levels this small factor each row with the whole CTA
 
 struct LuDev {
   const int32_t* sub_ptr;    // [n_sub + 1] block row ranges (concatenated)
@@ -70,6 +73,55 @@ __global__ void __launch_bounds__(LU_THREADS) k_lu_numeric(LuDev D, const double
   const double tol = 1e-14 * norm[s];
   for (int32_t lv = D.lev_sub[s]; lv < D.lev_sub[s + 1]; ++lv) {
     const int32_t r0 = D.lev_ptr[lv], r1 = D.lev_ptr[lv + 1];
+    if (r1 - r0 <= LU_COOP_ROWS) {
+      // few rows in this level (nested-dissection separators: one row per
+      // level): the whole CTA factors each row, the j updates of every k
+      // spread over all threads, one barrier per k (the k order and every
+      // w[j]'s subtraction order stay the reference's)
+      T* wc = wbuf + (size_t)s * LU_WARPS * D.n_max;
+      int32_t* sc = stamp_buf + (size_t)s * LU_WARPS * D.n_max;
+      for (int32_t t = r0; t < r1; ++t) {
+        const int32_t i = D.lev_rows[t];
+        const int32_t g = base + i;
+        const int64_t l0 = D.l_ptr[g], l1 = D.l_ptr[g + 1], u0 = D.u_ptr[g], u1 = D.u_ptr[g + 1];
+        for (int64_t p = l0 + threadIdx.x; p < l1; p += LU_THREADS) {
+          sc[D.l_idx[p]] = i;
+          wc[D.l_idx[p]] = T(0);
+        }
+        for (int64_t p = u0 + threadIdx.x; p < u1; p += LU_THREADS) {
+          sc[D.u_idx[p]] = i;
+          wc[D.u_idx[p]] = T(0);
+        }
+        __syncthreads();
+        for (int64_t p = D.ab_ptr[g] + threadIdx.x; p < D.ab_ptr[g + 1]; p += LU_THREADS) {
+          const int32_t j = D.ab_idx[p];
+          if (sc[j] == i) {
+            T v = (T)aval[D.ab_src[p]];
+            if (j == i && shift != T(0)) v = v + shift;
+            wc[j] = v;
+          }
+        }
+        __syncthreads();
+        for (int64_t p = l0; p < l1; ++p) {
+          const int32_t k = D.l_idx[p];
+          const int64_t k0 = D.u_ptr[base + k], k1 = D.u_ptr[base + k + 1];
+          // w[k] is final (its last update came from an earlier k, before
+          // the barrier) and never updated again: l_ik goes straight to L
+          const T lik = rn_div(wc[k], uval[k0]);
+          if (threadIdx.x == 0) lval[p] = lik;
+          for (int64_t q = k0 + 1 + threadIdx.x; q < k1; q += LU_THREADS) {
+            const int32_t j = D.u_idx[q];
+            if (sc[j] == i) wc[j] = rn_sub(wc[j], rn_mul(lik, uval[q]));
+          }
+          __syncthreads();
+        }
+        if (threadIdx.x == 0 && (double)fabs(wc[i]) <= tol)
+          atomicMin((unsigned long long*)(fail + s), (unsigned long long)(i + 1));
+        for (int64_t p = u0 + threadIdx.x; p < u1; p += LU_THREADS) uval[p] = wc[D.u_idx[p]];
+        __syncthreads();
+      }
+      continue;
+    }
     for (int32_t t = r0 + warp; t < r1; t += LU_WARPS) {
       const int32_t i = D.lev_rows[t];
       const int32_t g = base + i;
