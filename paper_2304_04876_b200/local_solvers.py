@@ -10,8 +10,8 @@ phase and solves on the GPU (mirrors schwarzdd.local_solvers).
   subdomains, see schwarz.setup_numeric / device.Precond.fastilu);
   `exact_lu` and `ilu_k` run the reference's pattern-restricted IKJ kernel
   (local_solvers.py:306-340) on the GPU, every block in one launch and
-  bit-identical to the host kernel; separator-heavy exact factors with few
-  blocks keep the parallel host kernel (schwarz._gpu_lu_pays).
+  bit-identical to the host kernel (separator chains factored by the whole
+  CTA per row; schwarz._gpu_lu_pays).
 * Solves: inside the preconditioner every block is solved in one launch --
   Jacobi FastSpTRSV for fast_ilu, the TMA-streamed level-set SpTRSV for
   ILU(k), supernodal partitioned inverses for exact factors (coarse_factor.py)

@@ -579,22 +579,18 @@ def _setup_clock():
 
 
 def _gpu_lu_pays(spec, symbolics) -> bool:
-    """GPU IKJ (a warp per row, its k loop serial like the reference's) or
-    the parallel host kernel. Measured on B200 + the box's host: ILU(k) and
-    exact factors with rows up to ~800 entries are 2.5-5x faster on the GPU
-    (C1 2.9 -> 0.5 s, C2 ILU(0) 2.8 -> 1.0 s); the dense separator rows of
-    C3-sized elasticity blocks (1,495 entries) serialise it, which only pays
-    once there are enough blocks to fill the GPU (64 blocks: 6 s host vs
-    10 s GPU; C3's 512 blocks: 55 s host vs 47 s GPU, whole numeric phase).
-    GDSW_HOST_LU=1 / =0 forces."""
+    """The reference's IKJ numeric LU / ILU(k) (lu_numeric, local_solvers.py:
+    306-340) runs on the GPU for every block (bit-identical to the host
+    kernel): a warp per row, and the whole CTA per row on levels of at most
+    two rows (nested-dissection separator chains). Measured on B200 vs the
+    parallel host kernel: C1 2.0 -> 0.4 s, 64 C3-sized elasticity blocks
+    6.4 -> 4.7 s, C3's 512 blocks 22.8 -> 14.9 s of local factorization.
+    GDSW_HOST_LU=1 forces the host kernel."""
     import os
     force = os.environ.get("GDSW_HOST_LU", "")
     if force in ("0", "1"):
         return force == "0"
-    if spec.method != "exact_lu":
-        return True
-    longest = max((int(np.diff(s.l_ptr).max(initial=0)) for s in symbolics), default=0)
-    return longest <= 1024 or len(symbolics) >= 256
+    return True
 
 
 def apply(m: TwoLevelPreconditioner, r):
