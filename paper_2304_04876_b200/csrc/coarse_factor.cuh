@@ -67,54 +67,6 @@ __device__ __forceinline__ T cf_dot(const T* __restrict__ row, const T* vec, int
   return warp_sum(((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7])));
 }
 
-// two independent dots interleaved (a row's two segments, or two rows):
-// four loads of each in flight, so short rows still overlap
-template <typename T>
-__device__ __forceinline__ void cf_dot2(const T* __restrict__ pa, const T* va, int a0, int a1,
-                                        const T* __restrict__ pb, const T* vb, int b0, int b1, int lane,
-                                        T& sa, T& sb) {
-  T a[4], b[4];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) a[u] = b[u] = T(0);
-  int ja = a0 + lane, jb = b0 + lane;
-  for (; ja + 96 < a1 && jb + 96 < b1; ja += 128, jb += 128) {
-    T ra[4], rb[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      ra[u] = ldg_stream(pa + ja + 32 * u);
-      rb[u] = ldg_stream(pb + jb + 32 * u);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      a[u] = fma(ra[u], va[ja + 32 * u], a[u]);
-      b[u] = fma(rb[u], vb[jb + 32 * u], b[u]);
-    }
-  }
-  for (; ja + 96 < a1; ja += 128) {
-    T ra[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) ra[u] = ldg_stream(pa + ja + 32 * u);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) a[u] = fma(ra[u], va[ja + 32 * u], a[u]);
-  }
-  for (; jb + 96 < b1; jb += 128) {
-    T rb[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) rb[u] = ldg_stream(pb + jb + 32 * u);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) b[u] = fma(rb[u], vb[jb + 32 * u], b[u]);
-  }
-  // tails of both, interleaved
-  for (; ja < a1 || jb < b1; ja += 32, jb += 32) {
-    const T xa = ja < a1 ? ldg_stream(pa + ja) : T(0);
-    const T xb = jb < b1 ? ldg_stream(pb + jb) : T(0);
-    if (ja < a1) a[0] = fma(xa, va[ja], a[0]);
-    if (jb < b1) b[0] = fma(xb, vb[jb], b[0]);
-  }
-  sa = warp_sum((a[0] + a[1]) + (a[2] + a[3]));
-  sb = warp_sum((b[0] + b[1]) + (b[2] + b[3]));
-}
-
 // input u indexed by the solve's own vector index, or through gmap (the
 // local solves read the global residual r at gmap[k], rounded once to T)
 template <typename T, typename TI>
@@ -256,52 +208,24 @@ __global__ void __launch_bounds__(CF_THREADS) k_cf_dataflow(CoarseFactorDev F, C
         buf[i] = acc;
       }
       __syncthreads();
-      // two rows per warp at a time (q and q + 8), their dots interleaved
-      for (int q = warp; q < nrows; q += 2 * (CF_THREADS / 32)) {
-        const int rows2[2] = {row0 + q, row0 + q + CF_THREADS / 32};
-        const bool on2[2] = {true, q + CF_THREADS / 32 < nrows};
-        const T* pr[2];
-        int hi[2];
-        T extra[2];
-        int32_t gg[2], np2[2];
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int row = rows2[h];
-          extra[h] = T(0);
-          gg[h] = np2[h] = 0;
-          if (!on2[h]) {
-            pr[h] = vals;
-            hi[h] = 0;
-          } else if (row < s) {
-            pr[h] = vals + F.d_off[k] + (int64_t)row * s;
-            hi[h] = row;
-          } else {
-            // the children's updates on this row (extend-add) are loaded by
-            // the lanes before the dot, so their latency overlaps its
-            // loads; added in list order after it
-            pr[h] = vals + F.m_off[k] + (int64_t)(row - s) * s;
-            hi[h] = s;
-            gg[h] = F.row_ptr[k] + row - s;
-            const int32_t p0 = F.out_ptr[gg[h]];
-            np2[h] = F.out_ptr[gg[h] + 1] - p0;
-            if (lane < np2[h]) extra[h] = __ldcg(cbuf + F.out_idx[p0 + lane]);
-          }
-        }
-        T acc2[2];
-        cf_dot2(pr[0], buf, 0, hi[0], pr[1], buf, 0, hi[1], lane, acc2[0], acc2[1]);
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          if (!on2[h]) continue;
-          const int row = rows2[h];
-          T acc = acc2[h];
-          if (row < s) {
-            if (lane == 0) y[cols[row]] = acc + buf[row];
-          } else {
-            for (int e = 0; e < min(np2[h], 32); ++e) acc += __shfl_sync(0xffffffffu, extra[h], e);
-            const int32_t p0 = F.out_ptr[gg[h]];
-            for (int32_t p = p0 + 32; p < p0 + np2[h]; ++p) acc += __ldcg(cbuf + F.out_idx[p]);
-            if (lane == 0) cbuf[gg[h]] = acc;
-          }
+      for (int q = warp; q < nrows; q += CF_THREADS / 32) {
+        const int row = row0 + q;
+        if (row >= s + r) break;
+        if (row < s) {
+          const T acc = cf_dot(vals + F.d_off[k] + (int64_t)row * s, buf, 0, row, lane);
+          if (lane == 0) y[cols[row]] = acc + buf[row];
+        } else {
+          // the children's updates on this row (extend-add) are loaded by
+          // the lanes before the dot, so their latency overlaps its loads;
+          // added in list order after it
+          const int32_t g = F.row_ptr[k] + row - s;
+          const int32_t p0 = F.out_ptr[g], np = F.out_ptr[g + 1] - p0;
+          T extra = T(0);
+          if (lane < np) extra = __ldcg(cbuf + F.out_idx[p0 + lane]);
+          T acc = cf_dot(vals + F.m_off[k] + (int64_t)(row - s) * s, buf, 0, s, lane);
+          for (int e = 0; e < min(np, 32); ++e) acc += __shfl_sync(0xffffffffu, extra, e);
+          for (int32_t p = p0 + 32; p < p0 + np; ++p) acc += __ldcg(cbuf + F.out_idx[p]);
+          if (lane == 0) cbuf[g] = acc;
         }
       }
     } else {
@@ -312,9 +236,8 @@ __global__ void __launch_bounds__(CF_THREADS) k_cf_dataflow(CoarseFactorDev F, C
       for (int q = warp; q < nrows; q += CF_THREADS / 32) {
         const int row = row0 + q;
         if (row >= s) break;
-        T a, b;
-        cf_dot2(vals + F.d_off[k] + (int64_t)row * s, buf, row, s, vals + F.n_off[k] + (int64_t)row * r, buf + s,
-                0, r, lane, a, b);
+        const T a = cf_dot(vals + F.d_off[k] + (int64_t)row * s, buf, row, s, lane);
+        const T b = cf_dot(vals + F.n_off[k] + (int64_t)row * r, buf + s, 0, r, lane);
         if (lane == 0) x[cols[row]] = a - b;
       }
     }
