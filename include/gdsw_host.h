@@ -111,13 +111,15 @@ int gh_classify_interface(int64_t n_nodes, const int64_t* g_ptr,
  * unz_off[b], in its own ND-permuted numbering; blk_base[b] = its offset in
  * the concatenated block vector. Result: {level_ptr, sn_s, sn_r, col_ptr,
  * col_ids, row_ptr, row_ids, d_off, m_off, n_off, values (f64), in_ptr,
- * in_idx, out_ptr, out_idx} -- include/gdsw.h gdsw_coarse_factor. */
+ * in_idx, out_ptr, out_idx} -- include/gdsw.h gdsw_coarse_factor. with_values = 0:
+ * the structure only (lv / uv unused, values empty; the device fills the
+ * blocks from its own factors, gdsw_precond_set_local_factor). */
 int gh_partitioned_inverse(int64_t nblk, const int64_t* blk_n, const int64_t* blk_base,
                            const int64_t* lp_off, const int64_t* lnz_off, const int64_t* up_off,
                            const int64_t* unz_off, const int64_t* lp, const int64_t* li,
                            const double* lv, const int64_t* up, const int64_t* ui,
                            const double* uv, int64_t relax, double zero_frac, int64_t threads,
-                           gh_result** out);
+                           int with_values, gh_result** out);
 
 #ifdef __cplusplus
 }

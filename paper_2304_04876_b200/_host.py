@@ -192,7 +192,8 @@ def overlap_sets(g_ptr, g_idx, node_owner, n_parts: int, subs, layers: int):
     return [nodes[ptr[k]:ptr[k + 1]] for k in range(subs.size)]
 
 
-def partitioned_inverse(blocks, relax: int, zero_frac: float, threads: int):
+def partitioned_inverse(blocks, relax: int, zero_frac: float, threads: int,
+                        with_values: bool = True):
     """Supernodal partitioned inverses of exact-LU blocks (gh_partitioned_inverse).
     blocks = [(base, l_ptr, l_idx, l_val, u_ptr, u_idx, u_val)]; returns the
     15 arrays of coarse_factor.CoarseFactor in ABI order."""
@@ -209,4 +210,5 @@ def partitioned_inverse(blocks, relax: int, zero_frac: float, threads: int):
     up, ui, uv = cat(4, np.int64), cat(5, np.int64), cat(6, np.float64)
     return _call(_lib.gh_partitioned_inverse, C.c_int64(nb), _p(blk_n), _p(base), _p(lp_off),
                  _p(lnz_off), _p(up_off), _p(unz_off), _p(lp), _p(li), _p(lv), _p(up), _p(ui),
-                 _p(uv), C.c_int64(relax), C.c_double(zero_frac), C.c_int64(threads))
+                 _p(uv), C.c_int64(relax), C.c_double(zero_frac), C.c_int64(threads),
+                 C.c_int(1 if with_values else 0))

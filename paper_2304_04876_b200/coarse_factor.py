@@ -60,6 +60,12 @@ class CoarseFactor:
     out_idx: np.ndarray
 
     @property
+    def n_values(self) -> int:
+        """Values of every supernode's D, M and N (also when `values` is
+        empty: a structure-only factor whose blocks the device computes)."""
+        return int(np.sum(self.sn_s * self.sn_s + 2 * self.sn_r * self.sn_s))
+
+    @property
     def n_levels(self) -> int:
         return self.level_ptr.size - 1
 
@@ -446,15 +452,18 @@ def _records_from_csr(lp, li, lv, up, ui, uv, keys, ids, max_zero_frac):
     return recs
 
 
-def build_block_factors(blocks, max_zero_frac: float = 0.3, threads: int = 0) -> CoarseFactor:
+def build_block_factors(blocks, max_zero_frac: float = 0.3, threads: int = 0,
+                        values: bool = True) -> CoarseFactor:
     """Partitioned inverses of many independent exact-LU local factors, one
     batch (supernodes of every block merged by tree level), built by the
     host runtime (libgdsw_host.so, threaded over blocks). `blocks` = list of
     (base, l_ptr, l_idx, l_val, u_ptr, u_idx, u_val): each block's CSR
     factors in its own (already ND-permuted) numbering -- L strictly lower
     with unit diagonal, U with the diagonal first -- and its offset in the
-    concatenated block vector. `build_block_factors_py` is the numpy
-    restatement the tests compare it with."""
+    concatenated block vector. values=False: the structure only (the value
+    arrays may be empty); the device fills the blocks from its own factors
+    (gdsw_precond_set_local_factor with values NULL). `build_block_factors_py`
+    is the numpy restatement the tests compare it with."""
     import os
     from . import _host
     if not threads:
@@ -463,7 +472,7 @@ def build_block_factors(blocks, max_zero_frac: float = 0.3, threads: int = 0) ->
                np.asarray(b[3], np.float64), np.asarray(b[4], np.int64),
                np.asarray(b[5], np.int64), np.asarray(b[6], np.float64)) for b in blocks]
     try:
-        arrs = _host.partitioned_inverse(blocks, RELAX, max_zero_frac, threads)
+        arrs = _host.partitioned_inverse(blocks, RELAX, max_zero_frac, threads, values)
     except RuntimeError as err:
         if "singular" in str(err):
             raise np.linalg.LinAlgError(str(err)) from err

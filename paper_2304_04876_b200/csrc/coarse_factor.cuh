@@ -274,4 +274,180 @@ __global__ void __launch_bounds__(CF_THREADS) k_cf_dataflow(CoarseFactorDev F, C
   }
 }
 
+// ---------------------------------------------------------------------------
+// numeric build of the local partitioned inverses ON THE DEVICE from the
+// device factors (the reference's IKJ LU, k_lu_numeric): the host computes
+// only the supernode structure from the symbolic patterns.
+//  k_pinv_fill   : thread per (supernode, stacked row): the row's CSR
+//                  entries that fall in the supernode go to its dense panels
+//                  [L_CC; L_RC] ((s + r) x s) and [U_CC, U_CR] (s x (s + r))
+//  k_pinv_blocks : CTA per supernode: L_CC^-1 (strict lower of D) and U_CC^-1
+//                  (upper of D) by row recurrences, then M = L_RC L_CC^-1 and
+//                  N = U_CC^-1 U_CR; fp64 arithmetic, stored in T
+// Row recurrences: row i of L^-1 = e_i - sum_{k<i} L[i][k] row_k; row i of
+// U^-1 = (e_i - sum_{k>i} U[i][k] row_k) / U[i][i] -- the host builder's.
+// ---------------------------------------------------------------------------
+constexpr int PB_THREADS = 256;
+constexpr int PB_J = 8;  // columns per thread: supernodes up to 2,048 columns
+
+struct PinvBuildDev {
+  const int64_t* l_ptr;     // factor CSR by global block position, block-local columns
+  const int32_t* l_idx;
+  const int64_t* u_ptr;
+  const int32_t* u_idx;
+  const int32_t* pos_sn;    // [n_loc] supernode owning each position (as a column)
+  const int32_t* pos_c;     // [n_loc] its index in that supernode's column list
+  const int32_t* sn_base;   // [n_sn] block base of each supernode
+  const int64_t* pan_off;   // [n_sn] offset of the L panel; the U panel follows it
+  const int2* rows;         // fill tasks: (supernode, stacked row)
+  int32_t n_rows;
+};
+
+template <typename T>
+__global__ void k_pinv_fill(CoarseFactorDev F, PinvBuildDev B, const T* __restrict__ lval,
+                            const T* __restrict__ uval, double* __restrict__ pan) {
+  const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B.n_rows) return;
+  const int2 task = B.rows[t];
+  const int q = task.x, rr = task.y;
+  const int s = F.sn_s[q], r = F.sn_r[q];
+  const int32_t base = B.sn_base[q];
+  const int32_t g = rr < s ? F.col_ids[F.col_ptr[q] + rr] : F.row_ids[F.row_ptr[q] + rr - s];
+  double* lp = pan + B.pan_off[q] + (int64_t)rr * s;
+  for (int64_t p = B.l_ptr[g]; p < B.l_ptr[g + 1]; ++p) {
+    const int32_t j = base + B.l_idx[p];
+    if (B.pos_sn[j] == q) lp[B.pos_c[j]] = (double)lval[p];
+  }
+  if (rr >= s) return;
+  double* up = pan + B.pan_off[q] + (int64_t)(s + r) * s + (int64_t)rr * (s + r);
+  const int32_t* R = F.row_ids + F.row_ptr[q];
+  for (int64_t p = B.u_ptr[g]; p < B.u_ptr[g + 1]; ++p) {
+    const int32_t j = base + B.u_idx[p];
+    if (B.pos_sn[j] == q) {
+      up[B.pos_c[j]] = (double)uval[p];
+    } else {
+      int lo = 0, hi = r;  // j is in R (the structure guarantees it)
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (R[mid] < j) lo = mid + 1; else hi = mid;
+      }
+      if (lo < r && R[lo] == j) up[s + lo] = (double)uval[p];
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(PB_THREADS) k_pinv_blocks(CoarseFactorDev F, PinvBuildDev B,
+                                                            const double* __restrict__ pan,
+                                                            double* __restrict__ dwork, T* __restrict__ vals,
+                                                            int32_t* __restrict__ bad) {
+  const int q = blockIdx.x;
+  const int s = F.sn_s[q], r = F.sn_r[q];
+  const double* L = pan + B.pan_off[q];              // (s + r) x s
+  const double* U = L + (int64_t)(s + r) * s;        // s x (s + r)
+  double* D = dwork + F.d_off[q];                    // s x s, fp64 scratch
+  const int tid = threadIdx.x;
+  // L_CC^-1 (strict lower of D; unit diagonal implied)
+  for (int i = 0; i < s; ++i) {
+    double acc[PB_J];
+#pragma unroll
+    for (int u = 0; u < PB_J; ++u) acc[u] = 0.0;
+    for (int k = 0; k < i; ++k) {
+      const double lik = L[(int64_t)i * s + k];
+      if (lik == 0.0) continue;
+#pragma unroll
+      for (int u = 0; u < PB_J; ++u) {
+        const int j = tid + PB_THREADS * u;
+        if (j <= k) acc[u] += lik * (j == k ? 1.0 : D[(int64_t)k * s + j]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PB_J; ++u) {
+      const int j = tid + PB_THREADS * u;
+      if (j < i) D[(int64_t)i * s + j] = -acc[u];
+    }
+    __syncthreads();
+  }
+  // U_CC^-1 (upper of D including the diagonal)
+  for (int i = s - 1; i >= 0; --i) {
+    const double dii = U[(int64_t)i * (s + r) + i];
+    if (dii == 0.0 || !isfinite(dii)) {
+      if (tid == 0) atomicExch(bad, 1);
+      return;
+    }
+    double acc[PB_J];
+#pragma unroll
+    for (int u = 0; u < PB_J; ++u) acc[u] = 0.0;
+    for (int k = i + 1; k < s; ++k) {
+      const double uik = U[(int64_t)i * (s + r) + k];
+      if (uik == 0.0) continue;
+#pragma unroll
+      for (int u = 0; u < PB_J; ++u) {
+        const int j = tid + PB_THREADS * u;
+        if (j >= k && j < s) acc[u] += uik * D[(int64_t)k * s + j];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PB_J; ++u) {
+      const int j = tid + PB_THREADS * u;
+      if (j == i) D[(int64_t)i * s + j] = 1.0 / dii;
+      else if (j > i && j < s) D[(int64_t)i * s + j] = -acc[u] / dii;
+    }
+    __syncthreads();
+  }
+  // M = L_RC L_CC^-1 (r x s): M[m][j] = L_R[m][j] + sum_{k > j} L_R[m][k] Linv[k][j]
+  T* M = vals + F.m_off[q];
+  for (int m = 0; m < r; ++m) {
+    const double* lr = L + (int64_t)(s + m) * s;
+    double acc[PB_J];
+#pragma unroll
+    for (int u = 0; u < PB_J; ++u) {
+      const int j = tid + PB_THREADS * u;
+      acc[u] = j < s ? lr[j] : 0.0;
+    }
+    for (int k = 1; k < s; ++k) {
+      const double a = lr[k];
+      if (a == 0.0) continue;
+#pragma unroll
+      for (int u = 0; u < PB_J; ++u) {
+        const int j = tid + PB_THREADS * u;
+        if (j < k) acc[u] += a * D[(int64_t)k * s + j];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < PB_J; ++u) {
+      const int j = tid + PB_THREADS * u;
+      if (j < s) M[(int64_t)m * s + j] = (T)acc[u];
+    }
+  }
+  // N = U_CC^-1 U_CR (s x r): N[i][m] = sum_{k >= i} Uinv[i][k] U_R[k][m]
+  T* N = vals + F.n_off[q];
+  for (int i = 0; i < s; ++i) {
+    for (int m0 = 0; m0 < r; m0 += PB_THREADS * PB_J) {
+      double acc[PB_J];
+#pragma unroll
+      for (int u = 0; u < PB_J; ++u) acc[u] = 0.0;
+      for (int k = i; k < s; ++k) {
+        const double a = D[(int64_t)i * s + k];
+        if (a == 0.0) continue;
+        const double* ur = U + (int64_t)k * (s + r) + s;
+#pragma unroll
+        for (int u = 0; u < PB_J; ++u) {
+          const int m = m0 + tid + PB_THREADS * u;
+          if (m < r) acc[u] += a * ur[m];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < PB_J; ++u) {
+        const int m = m0 + tid + PB_THREADS * u;
+        if (m < r) N[(int64_t)i * r + m] = (T)acc[u];
+      }
+    }
+  }
+  // D to the stored precision
+  T* Dv = vals + F.d_off[q];
+  __syncthreads();
+  for (int64_t e = tid; e < (int64_t)s * s; e += PB_THREADS) Dv[e] = (T)D[e];
+}
+
 }  // namespace gdsw

@@ -1676,8 +1676,12 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
   F.n_launch = 2 * nl;
   with_dtype(dtype, [&](auto tag) {
     using T = decltype(tag);
-    std::vector<double> h(f->values, f->values + f->n_values);
-    upload_cast<T>(F.vals, h);
+    if (f->values) {
+      std::vector<double> h(f->values, f->values + f->n_values);
+      upload_cast<T>(F.vals, h);
+    } else {
+      F.vals.alloc((size_t)std::max<int64_t>(f->n_values, 1) * sizeof(T));  // filled on the device
+    }
     F.ybuf.alloc((size_t)f->n * sizeof(T));
     F.cbuf.alloc((size_t)std::max<int64_t>(nrow, 1) * sizeof(T));
     // persistent grid: every CTA resident
@@ -1699,6 +1703,63 @@ int gdsw_precond_set_coarse_factor(gdsw_precond* m, const gdsw_coarse_factor* f)
   });
 }
 
+}  // extern "C"
+
+// the blocks of a structure-only partitioned inverse (values == NULL) from
+// the device factors: k_pinv_fill + k_pinv_blocks (coarse_factor.cuh)
+template <typename T>
+static void pinv_device_build(gdsw_precond* m, FactorBuf& F, const gdsw_coarse_factor* f) {
+  gdsw_plan* P = m->plan;
+  require(P->has_ab && m->has_factors, "device partitioned inverse needs the device factors (GPU LU)");
+  const int nsn = f->n_sn;
+  std::vector<int32_t> pos_sn(P->n_loc, -1), pos_c(P->n_loc, 0), sn_base(nsn);
+  std::vector<int64_t> pan_off(nsn);
+  std::vector<int2> rows;
+  int64_t pan = 0, smax = 0;
+  for (int q = 0; q < nsn; ++q) {
+    const int64_t s = f->sn_s[q], r = f->sn_r[q];
+    smax = std::max(smax, s);
+    for (int64_t c = 0; c < s; ++c) {
+      const int64_t g = f->col_ids[f->col_ptr[q] + c];
+      pos_sn[g] = q;
+      pos_c[g] = (int32_t)c;
+    }
+    const int64_t g0 = f->col_ids[f->col_ptr[q]];
+    const auto it = std::upper_bound(P->h_sub_ptr.begin(), P->h_sub_ptr.end(), g0);
+    sn_base[q] = (int32_t)*(it - 1);
+    pan_off[q] = pan;
+    pan += 2 * (s + r) * s;
+    for (int64_t t = 0; t < s + r; ++t) rows.push_back(make_int2(q, (int)t));
+  }
+  require(smax <= PB_THREADS * PB_J, "partitioned-inverse supernode too wide for the device build");
+  DBuf<int32_t> d_pos_sn, d_pos_c, d_sn_base;
+  DBuf<int64_t> d_pan_off;
+  DBuf<int2> d_rows;
+  d_pos_sn.upload(pos_sn);
+  d_pos_c.upload(pos_c);
+  d_sn_base.upload(sn_base);
+  d_pan_off.upload(pan_off);
+  d_rows.upload(rows);
+  DBuf<double> d_pan(std::max<int64_t>(pan, 1)), dwork(std::max<int64_t>(f->n_values, 1));
+  d_pan.zero();
+  DBuf<int32_t> bad(1);
+  bad.zero();
+  const PinvBuildDev B{P->l_ptr.p, P->l_idx32.p, P->u_ptr.p, P->u_idx32.p, d_pos_sn.p, d_pos_c.p,
+                       d_sn_base.p, d_pan_off.p, d_rows.p, (int32_t)rows.size()};
+  const CoarseFactorDev D = F.dev();
+  if (!rows.empty()) {
+    k_pinv_fill<T><<<grid_for((int64_t)rows.size(), TB), TB>>>(D, B, (const T*)m->lval.p, (const T*)m->uval.p,
+                                                               d_pan.p);
+    CK_LAUNCH();
+    k_pinv_blocks<T><<<nsn, PB_THREADS>>>(D, B, d_pan.p, dwork.p, (T*)F.vals.p, bad.p);
+    CK_LAUNCH();
+  }
+  CK(cudaDeviceSynchronize());
+  require(bad.download()[0] == 0, "matrix is singular", E_LINALG);
+}
+
+extern "C" {
+
 int gdsw_precond_set_local_factor(gdsw_precond* m, const gdsw_coarse_factor* f) {
   return guarded([&] {
     require(f == nullptr || f->n == m->plan->n_loc, "local factor dimension mismatch");
@@ -1706,6 +1767,8 @@ int gdsw_precond_set_local_factor(gdsw_precond* m, const gdsw_coarse_factor* f) 
       m->lf = FactorBuf{};
     } else {
       install_factor(m->lf, f, m->dtype, m->es);
+      if (!f->values)
+        with_dtype(m->dtype, [&](auto tag) { pinv_device_build<decltype(tag)>(m, m->lf, f); });
     }
     m->drop_graphs();
   });

@@ -971,7 +971,7 @@ void tri_inv_upper(i64 s, const std::vector<double>& a, std::vector<double>& inv
 }
 
 std::vector<PinvSn> pinv_block(i64 n, const i64* lp, const i64* li, const double* lv, const i64* up,
-                               const i64* ui, const double* uv, i64 relax, double zf) {
+                               const i64* ui, const double* uv, i64 relax, double zf, bool with_values) {
   // strictly lower symmetrized column structure
   std::vector<VI> col(n);
   for (i64 i = 0; i < n; ++i)
@@ -1087,6 +1087,7 @@ std::vector<PinvSn> pinv_block(i64 n, const i64* lp, const i64* li, const double
     if (!out[q].rows.empty()) out[q].parent = newid[find(sn_of[out[q].rows[0]])];
   for (i64 q = 0; q < nq; ++q)
     if (out[q].parent >= 0) out[out[q].parent].level = std::max(out[out[q].parent].level, out[q].level + 1);
+  if (!with_values) return out;  // structure only (the device computes the blocks)
   // panels [L_CC; L_RC] ((s + r) x s) and [U_CC, U_CR] (s x (s + r))
   std::vector<std::vector<double>> lpan(nq), upan(nq);
   for (i64 q = 0; q < nq; ++q) {
@@ -1166,7 +1167,7 @@ extern "C" int gh_partitioned_inverse(int64_t nblk, const int64_t* blk_n, const 
                                       const int64_t* unz_off, const int64_t* lp, const int64_t* li,
                                       const double* lv, const int64_t* up, const int64_t* ui,
                                       const double* uv, int64_t relax, double zero_frac, int64_t threads,
-                                      gh_result** res) {
+                                      int with_values, gh_result** res) {
   GH_TRY({
     std::vector<std::vector<PinvSn>> per(nblk);
     std::vector<std::string> errs(nblk);
@@ -1176,8 +1177,9 @@ extern "C" int gh_partitioned_inverse(int64_t nblk, const int64_t* blk_n, const 
         const i64 b = next.fetch_add(1);
         if (b >= nblk) break;
         try {
-          per[b] = pinv_block(blk_n[b], lp + lp_off[b], li + lnz_off[b], lv + lnz_off[b], up + up_off[b],
-                              ui + unz_off[b], uv + unz_off[b], relax, zero_frac);
+          per[b] = pinv_block(blk_n[b], lp + lp_off[b], li + lnz_off[b], with_values ? lv + lnz_off[b] : nullptr,
+                              up + up_off[b], ui + unz_off[b], with_values ? uv + unz_off[b] : nullptr, relax,
+                              zero_frac, with_values != 0);
         } catch (const std::exception& e) {
           errs[b] = e.what();
         }
@@ -1221,15 +1223,16 @@ extern "C" int gh_partitioned_inverse(int64_t nblk, const int64_t* blk_n, const 
       const i64 base = blk_base[ord[t].b];
       for (i64 c = 0; c < sn_s[t]; ++c) col_ids[col_ptr[t] + c] = base + o.cols[c];
       for (i64 c = 0; c < sn_r[t]; ++c) row_ids[row_ptr[t] + c] = base + o.rows[c];
+      const i64 s_ = sn_s[t], r_ = sn_r[t];
       d_off[t] = nval;
-      nval += (i64)o.d.size();
+      nval += s_ * s_;
       m_off[t] = nval;
-      nval += (i64)o.m.size();
+      nval += r_ * s_;
       n_off[t] = nval;
-      nval += (i64)o.nm.size();
+      nval += s_ * r_;
     }
-    std::vector<double> vals((size_t)nval);
-    for (i64 t = 0; t < nsn; ++t) {
+    std::vector<double> vals(with_values ? (size_t)nval : (size_t)0);
+    for (i64 t = 0; t < nsn && with_values; ++t) {
       const PinvSn& o = per[ord[t].b][ord[t].q];
       std::copy(o.d.begin(), o.d.end(), vals.begin() + d_off[t]);
       std::copy(o.m.begin(), o.m.end(), vals.begin() + m_off[t]);

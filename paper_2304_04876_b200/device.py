@@ -385,8 +385,10 @@ class Precond:
     def _factor_desc(f):
         keep = {k: np.ascontiguousarray(getattr(f, k), dtype=np.int64) for k in _CF_ARRAYS}
         vals = np.ascontiguousarray(f.values, dtype=np.float64)
-        d = _CoarseFactor(n=f.n, n_sn=f.n_sn, n_levels=f.n_levels, values=vals.ctypes.data,
-                          n_values=vals.size, **{k: v.ctypes.data for k, v in keep.items()})
+        # no values: a structure-only factor, the device computes its blocks
+        d = _CoarseFactor(n=f.n, n_sn=f.n_sn, n_levels=f.n_levels,
+                          values=vals.ctypes.data if vals.size else None,
+                          n_values=f.n_values, **{k: v.ctypes.data for k, v in keep.items()})
         return d, (keep, vals)
 
     def set_coarse_factor(self, f):

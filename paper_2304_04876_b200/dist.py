@@ -182,7 +182,8 @@ class DistPreconditioner:
                 uvs.append(uv)
             self.pre.set_factors(np.concatenate(lvs).astype(vdt), np.concatenate(uvs).astype(vdt))
         if spec.method == "exact_lu" and _local_factor_pays(syms):
-            _install_local_factor(self.pre, self.plan, syms)
+            _install_local_factor(self.pre, self.plan, syms,
+                                  on_device=self.plan.has_block_pattern and _gpu_lu_pays(spec, syms))
         self.coarse_n = 0
         if config.use_coarse:
             self._coarse(a, coarse_src, a_ext, a_ext_dev, dec, nullspace, config, single,

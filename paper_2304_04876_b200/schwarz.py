@@ -485,7 +485,8 @@ def setup_numeric(skeleton: PreconditionerSkeleton, a: CsrMatrix,
 
     tick("local factors")
     if spec.method == "exact_lu" and _local_factor_pays(skeleton.local_symbolics):
-        _install_local_factor(pre, plan, skeleton.local_symbolics)
+        _install_local_factor(pre, plan, skeleton.local_symbolics,
+                              on_device=plan.has_block_pattern and _gpu_lu_pays(spec, []))
         tick("local partitioned inverses")
     coarse = None
     if config.use_coarse:
@@ -548,18 +549,28 @@ def _local_factor_pays(syms) -> bool:
     return not many and fill <= 2_000_000_000 and max(s.n for s in syms) <= 20_000
 
 
-def _install_local_factor(pre, plan, syms):
+def _install_local_factor(pre, plan, syms, on_device: bool = True):
+    """Partitioned inverses of the exact local factors. on_device: the host
+    derives only the supernode structure from the symbolic patterns and the
+    device computes the blocks from its own factors (k_pinv_fill /
+    k_pinv_blocks); else the host runtime computes them from downloaded
+    factors (GDSW_PINV_HOST=1)."""
+    import os
     from .coarse_factor import build_block_factors
-    lv, uv = pre.factors(plan.nnz_l, plan.nnz_u)
+    on_device = on_device and os.environ.get("GDSW_PINV_HOST") != "1"
+    if on_device:
+        lv = uv = np.zeros(0)
+    else:
+        lv, uv = pre.factors(plan.nnz_l, plan.nnz_u)
     blocks, base, lo, uo = [], 0, 0, 0
     for sym in syms:
         nl, nu = sym.l_idx.size, sym.u_idx.size
-        blocks.append((base, sym.l_ptr, sym.l_idx, lv[lo:lo + nl], sym.u_ptr, sym.u_idx,
-                       uv[uo:uo + nu]))
+        blocks.append((base, sym.l_ptr, sym.l_idx, lv[lo:lo + nl] if lv.size else lv, sym.u_ptr,
+                       sym.u_idx, uv[uo:uo + nu] if uv.size else uv))
         base += sym.n
         lo += nl
         uo += nu
-    pre.set_local_factor(build_block_factors(blocks))
+    pre.set_local_factor(build_block_factors(blocks, values=not on_device))
 
 
 def _setup_clock():

@@ -116,6 +116,12 @@ def test_block_factors_match_levelset_solves(name):
               "m_off", "n_off", "in_ptr", "in_idx", "out_ptr", "out_idx"):
         assert np.array_equal(getattr(f, k), getattr(fp, k)), k
     assert np.abs(f.values - fp.values).max() <= 1e-12 * np.abs(fp.values).max()
+    # structure-only build (the device computes the blocks): same structure
+    fs = build_block_factors(blocks, threads=2, values=False)
+    for k in ("level_ptr", "sn_s", "sn_r", "col_ptr", "col_ids", "row_ptr", "row_ids", "d_off",
+              "m_off", "n_off", "in_ptr", "in_idx", "out_ptr", "out_idx"):
+        assert np.array_equal(getattr(f, k), getattr(fs, k)), k
+    assert fs.values.size == 0 and fs.n_values == f.values.size
     rng = np.random.default_rng(7)
     b = rng.standard_normal(base)
     x = solve_host(f, b)

@@ -386,6 +386,33 @@ def test_iteration_counts_at_size(golden, name):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name", ["lap9_exact_nd", "ela7_exact"])
+def test_local_partitioned_inverse_device_build_matches_host(monkeypatch, name):
+    """Exact-LU local solves through partitioned inverses whose blocks the
+    device computes (k_pinv_fill / k_pinv_blocks, from its own factors)
+    against the host runtime's blocks (1e-13 relative per block), and both
+    against the streamed level-set substitution."""
+    torch = _torch()
+    out = {}
+    for mode, env in (("device", {}), ("host", {"GDSW_PINV_HOST": "1"}),
+                      ("stream", {"GDSW_LOCAL_FACTOR": "0"})):
+        for k in ("GDSW_PINV_HOST", "GDSW_LOCAL_FACTOR"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        prob, dec, cfg = build(PKG, CASES[name])
+        skel = sw.setup_symbolic(prob.a, dec, cfg)
+        pre = sw.setup_numeric(skel, prob.a, prob.nullspace if cfg.use_coarse else None)
+        r = probes(prob.a.nrows, ks=(5,))[0]
+        y = torch.empty(skel._local_plan["n_loc"], dtype=torch.float64, device="cuda")
+        pre._dev.local_solve(torch.from_numpy(r).cuda(), y)
+        out[mode] = y.cpu().numpy()
+    scale = np.abs(out["stream"]).max()
+    assert np.abs(out["device"] - out["host"]).max() <= 1e-13 * scale
+    assert np.abs(out["device"] - out["stream"]).max() <= LONG_ROW_TOL * scale
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("precision", ["double", "single"])
 def test_factored_coarse_solve_matches_dense_inverse(monkeypatch, precision):
     """The factored coarse solve (supernodal partitioned inverse, one launch
