@@ -43,7 +43,13 @@ struct CoarseFactorDev {
   const int32_t* in_idx;
   const int32_t* out_ptr;  // by flattened update row (row_ptr order)
   const int32_t* out_idx;
+  // narrow supernodes (s <= CF_CM_MAX): the forward block [L_kk^-1; M] also
+  // stored column-major ((s + r) x s, column c contiguous over the rows), so
+  // a thread per row streams it coalesced with no reduction; -1 otherwise
+  const int64_t* f_off;
 };
+
+constexpr int CF_CM_MAX = 128;
 
 // dot of a dense row segment [j0, j1) with a shared-memory vector: lanes
 // over the columns, eight independent partial sums (eight row loads in
@@ -154,15 +160,34 @@ __device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t* p) {
   return v;
 }
 
+// column-major forward panel of the narrow supernodes, from D (strict lower)
+// and M: F[c (s + r) + i] = L_kk^-1[i][c] (i < s, zero on and above the
+// diagonal), M[i - s][c] (i >= s)
+template <typename T>
+__global__ void k_pinv_fcm(CoarseFactorDev F, const int32_t* __restrict__ sn_list, int32_t n_list,
+                           const T* __restrict__ vals, T* __restrict__ fcm) {
+  const int q = sn_list[blockIdx.x];
+  const int s = F.sn_s[q], r = F.sn_r[q];
+  const T* D = vals + F.d_off[q];
+  const T* M = vals + F.m_off[q];
+  T* out = fcm + F.f_off[q];
+  for (int64_t e = threadIdx.x; e < (int64_t)(s + r) * s; e += blockDim.x) {
+    const int c = (int)(e / (s + r)), i = (int)(e % (s + r));
+    out[e] = i < s ? (c < i ? D[(int64_t)i * s + c] : T(0)) : M[(int64_t)(i - s) * s + c];
+  }
+}
+
 template <typename T, typename TI>
 __global__ void __launch_bounds__(CF_THREADS) k_cf_dataflow(CoarseFactorDev F, CfSched S,
                                                             const int2* __restrict__ tasks,
                                                             const T* __restrict__ vals, const TI* __restrict__ u,
                                                             const int32_t* __restrict__ gmap, T* __restrict__ y,
-                                                            T* __restrict__ cbuf, T* __restrict__ x) {
+                                                            T* __restrict__ cbuf, T* __restrict__ x,
+                                                            const T* __restrict__ fcm) {
   extern __shared__ __align__(16) unsigned char cf_sm[];
   T* buf = reinterpret_cast<T*>(cf_sm);
   __shared__ int32_t cur;
+  __shared__ T red[CF_THREADS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // thread 0 holds the next ticket while the CTA works on the current one
   // (no deadlock: the smallest unfinished ticket is always either running
@@ -208,6 +233,41 @@ __global__ void __launch_bounds__(CF_THREADS) k_cf_dataflow(CoarseFactorDev F, C
         buf[i] = acc;
       }
       __syncthreads();
+      if (F.f_off[k] >= 0) {
+        // narrow supernode: thread per row over the column-major panel, the
+        // columns split in two halves (threads t and t + 128) combined in order
+        const T* P = fcm + F.f_off[k];
+        const int half = threadIdx.x / (CF_THREADS / 2), q = threadIdx.x % (CF_THREADS / 2);
+        const int row = row0 + q;
+        const bool on = q < nrows;
+        const int c0 = half ? s / 2 : 0, c1 = half ? s : s / 2;
+        T extra = T(0);
+        int32_t gi = -1;
+        if (on && half == 0 && row >= s) {  // extend-add terms, loaded ahead
+          gi = F.row_ptr[k] + row - s;
+          for (int32_t p = F.out_ptr[gi]; p < F.out_ptr[gi + 1]; ++p) extra += __ldcg(cbuf + F.out_idx[p]);
+        }
+        T a[4] = {T(0), T(0), T(0), T(0)};
+        if (on) {
+          const T* pc = P + row;
+          int c = c0;
+          for (; c + 4 <= c1; c += 4) {
+            T v[4];
+#pragma unroll
+            for (int uu = 0; uu < 4; ++uu) v[uu] = ldg_stream(pc + (int64_t)(c + uu) * (s + r));
+#pragma unroll
+            for (int uu = 0; uu < 4; ++uu) a[uu] = fma(v[uu], buf[c + uu], a[uu]);
+          }
+          for (; c < c1; ++c) a[0] = fma(ldg_stream(pc + (int64_t)c * (s + r)), buf[c], a[0]);
+        }
+        red[threadIdx.x] = (a[0] + a[1]) + (a[2] + a[3]);
+        __syncthreads();
+        if (on && half == 0) {
+          const T acc = red[threadIdx.x] + red[threadIdx.x + CF_THREADS / 2];
+          if (row < s) y[cols[row]] = acc + buf[row];
+          else cbuf[gi] = acc + extra;
+        }
+      } else
       for (int q = warp; q < nrows; q += CF_THREADS / 32) {
         const int row = row0 + q;
         if (row >= s + r) break;

@@ -576,12 +576,15 @@ struct FactorBuf {
   size_t df_smem = 0;
   std::vector<int32_t> fwd_ptr, bwd_ptr;  // per level: task ranges (forward, backward)
   std::vector<size_t> fwd_smem, bwd_smem;
-  DBuf<char> vals, ybuf, cbuf;
+  DBuf<char> vals, ybuf, cbuf, fcm;
+  DBuf<int64_t> f_off;
+  DBuf<int32_t> cm_list;
+  int32_t n_cm = 0;
   int64_t bytes = 0, n_launch = 0;
   CoarseFactorDev dev() const {
     return CoarseFactorDev{parent.p, child_ptr.p, child_idx.p, fwd_need.p, bwd_need.p,
                            sn_s.p, sn_r.p, col_ptr.p, col_ids.p, row_ptr.p, row_ids.p,
-                           d_off.p, m_off.p, n_off.p, in_ptr.p, in_idx.p, out_ptr.p, out_idx.p};
+                           d_off.p, m_off.p, n_off.p, in_ptr.p, in_idx.p, out_ptr.p, out_idx.p, f_off.p};
   }
 };
 
@@ -874,7 +877,8 @@ void factor_solve(const FactorBuf& F, const TI* u, const int32_t* gmap, T* x, cu
     // one launch: dependency-driven tiles (k_cf_dataflow)
     CfSched S{F.ticket.p, F.ready.p, F.ready.p + F.n_sn, F.n_fwd_tasks, F.n_df_tasks, F.n_sn};
     k_cf_dataflow<T, TI><<<F.df_grid, CF_THREADS, F.df_smem, s>>>(D, S, F.df_tasks.p, (const T*)F.vals.p, u,
-                                                                   gmap, (T*)F.ybuf.p, (T*)F.cbuf.p, x);
+                                                                   gmap, (T*)F.ybuf.p, (T*)F.cbuf.p, x,
+                                                                   (const T*)F.fcm.p);
     CK_LAUNCH();
     return;
   }
@@ -1532,6 +1536,18 @@ int gdsw_precond_set_coarse_inverse(gdsw_precond* m, const double* a0inv) {
   });
 }
 
+}  // extern "C"
+
+template <typename T>
+static void build_fcm(FactorBuf& F) {
+  if (F.n_cm == 0) return;
+  k_pinv_fcm<T><<<F.n_cm, 256>>>(F.dev(), F.cm_list.p, F.n_cm, (const T*)F.vals.p, (T*)F.fcm.p);
+  CK_LAUNCH();
+  CK(cudaDeviceSynchronize());
+}
+
+extern "C" {
+
 // upload a host partitioned inverse (gdsw_coarse_factor) into F in the
 // precond dtype; tasks are CF_ROWS-row tiles of each supernode's stacked
 // rows (forward: s + r, backward: s)
@@ -1552,6 +1568,23 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
   F.d_off.upload(f->d_off, nsn);
   F.m_off.upload(f->m_off, nsn);
   F.n_off.upload(f->n_off, nsn);
+  {
+    // narrow supernodes get a column-major copy of their forward block
+    static const bool cm_off = env_flag("GDSW_CF_NOCM");
+    std::vector<int64_t> foff(nsn, -1);
+    std::vector<int32_t> cm;
+    int64_t tot = 0;
+    for (int k = 0; k < nsn; ++k)
+      if (!cm_off && f->sn_s[k] <= CF_CM_MAX && f->sn_s[k] > 0) {
+        foff[k] = tot;
+        tot += (f->sn_s[k] + f->sn_r[k]) * f->sn_s[k];
+        cm.push_back(k);
+      }
+    F.f_off.upload(foff);
+    F.cm_list.upload(cm.empty() ? std::vector<int32_t>{0} : cm);
+    F.n_cm = (int32_t)cm.size();
+    F.fcm.alloc((size_t)std::max<int64_t>(tot, 1) * es);
+  }
   std::vector<int2> tasks;
   F.fwd_ptr.assign(1, 0);
   F.fwd_smem.assign(nl, 0);
@@ -1679,6 +1712,7 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
     if (f->values) {
       std::vector<double> h(f->values, f->values + f->n_values);
       upload_cast<T>(F.vals, h);
+      build_fcm<T>(F);
     } else {
       F.vals.alloc((size_t)std::max<int64_t>(f->n_values, 1) * sizeof(T));  // filled on the device
     }
@@ -1756,6 +1790,7 @@ static void pinv_device_build(gdsw_precond* m, FactorBuf& F, const gdsw_coarse_f
   }
   CK(cudaDeviceSynchronize());
   require(bad.download()[0] == 0, "matrix is singular", E_LINALG);
+  build_fcm<T>(F);
 }
 
 extern "C" {

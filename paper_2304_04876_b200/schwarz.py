@@ -541,12 +541,10 @@ def _local_factor_pays(syms) -> bool:
     if force in ("0", "1"):
         return force == "1"
     fill = sum(s.l_idx.size + s.u_idx.size for s in syms)
-    # measured (B200): C1's 8 blocks 0.86 -> 0.16 ms, 64 C3-sized blocks
-    # 1.43 -> 0.44 ms per local solve; C3's 512 blocks: on par with the
-    # streamed SpTRSV (3.5 vs 3.3 ms), which keeps three CTAs per SM there
-    from . import device
-    many = len(syms) > 2 * device.torch().cuda.get_device_properties(0).multi_processor_count
-    return not many and fill <= 2_000_000_000 and max(s.n for s in syms) <= 20_000
+    # measured (B200) against the streamed level-set SpTRSV: C1's 8 blocks
+    # 0.86 -> 0.15 ms, 64 C3-sized blocks 1.43 -> 0.33 ms, C3's 512 blocks
+    # 3.3 -> 2.5 ms per local solve (C3 solve 151 -> 115 ms)
+    return fill <= 2_000_000_000 and max(s.n for s in syms) <= 20_000
 
 
 def _install_local_factor(pre, plan, syms, on_device: bool = True):

@@ -1,0 +1,8 @@
+# round 2: column-major forward blocks for narrow supernodes
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "local_solves or golden or factored or partitioned or supernodal" > gpurun_out/r2w_parity.log 2>&1
+for nocm in 0 1 0; do
+  for c in C1 C3s; do GDSW_CF_NOCM=$nocm timeout 900 python tools/profile_ts.py $c 30 2>&1 | grep "local solve" | sed "s/^/nocm $nocm: /" >> gpurun_out/r2w_ts.log; done
+  GDSW_CF_NOCM=$nocm GDSW_COARSE_FACTOR=1 timeout 600 python tools/profile_coarse.py 16 16 8 2>&1 | sed "s/^/nocm $nocm: /" >> gpurun_out/r2w_ts.log
+done
+GDSW_LOCAL_FACTOR=1 timeout 1200 python tools/run_configs.py C3 > gpurun_out/r2w_c3.jsonl 2> gpurun_out/r2w_c3.err

@@ -50,6 +50,9 @@ int main() {
       run<16, 1>(mult * sms / 2, n, V, ld, nt, v, z, part, out, ctr, "");
       run<16, 2>(mult * sms / 2, n, V, ld, nt, v, z, part, out, ctr, "");
     }
+    for (int nt : {20, 24}) run<24, 1>(mult * sms / 2, n, V, ld, nt, v, z, part, out, ctr, "");
+    for (int nt : {28, 31}) run<32, 1>(mult * sms / 2, n, V, ld, nt, v, z, part, out, ctr, "");
+    for (int nt : {20, 24}) run<16, 1>(mult * sms / 2, n, V, ld, 16, v, z, part, out, ctr, "split16");
   }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
 }
