@@ -175,6 +175,14 @@ __global__ void k_pinv_fcm(CoarseFactorDev F, const int32_t* __restrict__ sn_lis
     const int c = (int)(e / (s + r)), i = (int)(e % (s + r));
     out[e] = i < s ? (c < i ? D[(int64_t)i * s + c] : T(0)) : M[(int64_t)(i - s) * s + c];
   }
+  // backward block [U_kk^-1 | -N] column-major (s rows, s + r columns):
+  // B[c s + i] = U_kk^-1[i][c] (c >= i, else 0), -N[i][c - s] (c >= s)
+  const T* N = vals + F.n_off[q];
+  T* bo = out + (int64_t)(s + r) * s;
+  for (int64_t e = threadIdx.x; e < (int64_t)(s + r) * s; e += blockDim.x) {
+    const int c = (int)(e / s), i = (int)(e % s);
+    bo[e] = c < s ? (c >= i ? D[(int64_t)i * s + c] : T(0)) : -N[(int64_t)i * r + (c - s)];
+  }
 }
 
 template <typename T, typename TI>
@@ -234,13 +242,17 @@ __global__ void __launch_bounds__(CF_THREADS) k_cf_dataflow(CoarseFactorDev F, C
       }
       __syncthreads();
       if (F.f_off[k] >= 0) {
-        // narrow supernode: thread per row over the column-major panel, the
-        // columns split in two halves (threads t and t + 128) combined in order
+        // narrow supernode: thread per row over the column-major panel; the
+        // columns split in `spl` contiguous parts (spl = 256 / rows rounded
+        // down to a power of two) whose partials are combined in part order
         const T* P = fcm + F.f_off[k];
-        const int half = threadIdx.x / (CF_THREADS / 2), q = threadIdx.x % (CF_THREADS / 2);
+        int spl = 2;
+        while (spl < 16 && nrows * spl * 2 <= CF_THREADS) spl *= 2;
+        const int rows_pad = CF_THREADS / spl;
+        const int half = threadIdx.x / rows_pad, q = threadIdx.x % rows_pad;
         const int row = row0 + q;
         const bool on = q < nrows;
-        const int c0 = half ? s / 2 : 0, c1 = half ? s : s / 2;
+        const int c0 = (int)((int64_t)s * half / spl), c1 = (int)((int64_t)s * (half + 1) / spl);
         T extra = T(0);
         int32_t gi = -1;
         if (on && half == 0 && row >= s) {  // extend-add terms, loaded ahead
@@ -263,7 +275,8 @@ __global__ void __launch_bounds__(CF_THREADS) k_cf_dataflow(CoarseFactorDev F, C
         red[threadIdx.x] = (a[0] + a[1]) + (a[2] + a[3]);
         __syncthreads();
         if (on && half == 0) {
-          const T acc = red[threadIdx.x] + red[threadIdx.x + CF_THREADS / 2];
+          T acc = red[threadIdx.x];
+          for (int h = 1; h < spl; ++h) acc += red[threadIdx.x + h * rows_pad];
           if (row < s) y[cols[row]] = acc + buf[row];
           else cbuf[gi] = acc + extra;
         }
@@ -293,6 +306,40 @@ __global__ void __launch_bounds__(CF_THREADS) k_cf_dataflow(CoarseFactorDev F, C
       for (int i = threadIdx.x; i < s + r; i += CF_THREADS)
         buf[i] = i < s ? __ldcg(y + cols[i]) : __ldcg(x + rows[i - s]);
       __syncthreads();
+      if (F.f_off[k] >= 0) {
+        // narrow supernode: thread per row over the column-major [U^-1 | -N],
+        // the s + r columns split in `spl` parts combined in part order
+        const T* P = fcm + F.f_off[k] + (int64_t)(s + r) * s;
+        int spl = 2;
+        while (spl < 16 && nrows * spl * 2 <= CF_THREADS) spl *= 2;
+        const int rows_pad = CF_THREADS / spl;
+        const int part = threadIdx.x / rows_pad, q = threadIdx.x % rows_pad;
+        const int row = row0 + q;
+        const bool on = q < nrows;
+        const int w = s + r;
+        const int c0 = max((int)((int64_t)w * part / spl), on ? row : 0);
+        const int c1 = (int)((int64_t)w * (part + 1) / spl);
+        T a[4] = {T(0), T(0), T(0), T(0)};
+        if (on) {
+          const T* pc = P + row;
+          int c = c0;
+          for (; c + 4 <= c1; c += 4) {
+            T v[4];
+#pragma unroll
+            for (int uu = 0; uu < 4; ++uu) v[uu] = ldg_stream(pc + (int64_t)(c + uu) * s);
+#pragma unroll
+            for (int uu = 0; uu < 4; ++uu) a[uu] = fma(v[uu], buf[c + uu], a[uu]);
+          }
+          for (; c < c1; ++c) a[0] = fma(ldg_stream(pc + (int64_t)c * s), buf[c], a[0]);
+        }
+        red[threadIdx.x] = (a[0] + a[1]) + (a[2] + a[3]);
+        __syncthreads();
+        if (on && part == 0) {
+          T acc = red[threadIdx.x];
+          for (int h = 1; h < spl; ++h) acc += red[threadIdx.x + h * rows_pad];
+          x[cols[row]] = acc;
+        }
+      } else
       for (int q = warp; q < nrows; q += CF_THREADS / 32) {
         const int row = row0 + q;
         if (row >= s) break;

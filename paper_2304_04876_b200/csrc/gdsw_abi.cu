@@ -1577,7 +1577,7 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
     for (int k = 0; k < nsn; ++k)
       if (!cm_off && f->sn_s[k] <= CF_CM_MAX && f->sn_s[k] > 0) {
         foff[k] = tot;
-        tot += (f->sn_s[k] + f->sn_r[k]) * f->sn_s[k];
+        tot += 2 * (f->sn_s[k] + f->sn_r[k]) * f->sn_s[k];   // forward + backward panels
         cm.push_back(k);
       }
     F.f_off.upload(foff);
