@@ -49,7 +49,12 @@ struct CoarseFactorDev {
   const int64_t* f_off;
 };
 
+// widest supernode with column-major panels: coarse factors 128, local
+// exact-LU blocks 512 (measured: C3-sized blocks 0.311 -> 0.298 ms with 512;
+// the n_c = 12,600 coarse solve 0.287 -> 0.298 ms, so it keeps 128);
+// GDSW_CF_CM_MAX overrides both
 constexpr int CF_CM_MAX = 128;
+constexpr int CF_CM_LOCAL = 512;
 
 // dot of a dense row segment [j0, j1) with a shared-memory vector: lanes
 // over the columns, eight independent partial sums (eight row loads in

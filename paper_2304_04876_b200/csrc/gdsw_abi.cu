@@ -1551,7 +1551,7 @@ extern "C" {
 // upload a host partitioned inverse (gdsw_coarse_factor) into F in the
 // precond dtype; tasks are CF_ROWS-row tiles of each supernode's stacked
 // rows (forward: s + r, backward: s)
-static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype, size_t es) {
+static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype, size_t es, int64_t cm_default) {
   const int nsn = f->n_sn, nl = f->n_levels;
   auto i32 = [](const int64_t* a, size_t n) { return to_i32(a, n); };
   F.sn_s.upload(i32(f->sn_s, nsn));
@@ -1571,11 +1571,16 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
   {
     // narrow supernodes get a column-major copy of their forward block
     static const bool cm_off = env_flag("GDSW_CF_NOCM");
+    static const int64_t cm_env = [] {
+      const char* e = std::getenv("GDSW_CF_CM_MAX");
+      return e ? (int64_t)std::atoi(e) : (int64_t)-1;
+    }();
+    const int64_t cm_max = cm_env >= 0 ? cm_env : cm_default;
     std::vector<int64_t> foff(nsn, -1);
     std::vector<int32_t> cm;
     int64_t tot = 0;
     for (int k = 0; k < nsn; ++k)
-      if (!cm_off && f->sn_s[k] <= CF_CM_MAX && f->sn_s[k] > 0) {
+      if (!cm_off && f->sn_s[k] <= cm_max && f->sn_s[k] > 0) {
         foff[k] = tot;
         tot += 2 * (f->sn_s[k] + f->sn_r[k]) * f->sn_s[k];   // forward + backward panels
         cm.push_back(k);
@@ -1730,7 +1735,7 @@ int gdsw_precond_set_coarse_factor(gdsw_precond* m, const gdsw_coarse_factor* f)
   return guarded([&] {
     require(m->cp != nullptr, "preconditioner has no coarse structure");
     require(f->n == m->cp->n_c, "coarse factor dimension mismatch");
-    install_factor(m->cf, f, m->dtype, m->es);
+    install_factor(m->cf, f, m->dtype, m->es, CF_CM_MAX);
     m->ainv.release();
     m->has_ainv = true;
     m->drop_graphs();
@@ -1801,7 +1806,7 @@ int gdsw_precond_set_local_factor(gdsw_precond* m, const gdsw_coarse_factor* f) 
     if (f == nullptr) {
       m->lf = FactorBuf{};
     } else {
-      install_factor(m->lf, f, m->dtype, m->es);
+      install_factor(m->lf, f, m->dtype, m->es, CF_CM_LOCAL);
       if (!f->values)
         with_dtype(m->dtype, [&](auto tag) { pinv_device_build<decltype(tag)>(m, m->lf, f); });
     }
