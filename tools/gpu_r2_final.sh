@@ -1,6 +1,6 @@
 # round 2 evidence: full GPU suite, smoke, bench (+ reference arm), configs, ncu launch list + captures
 mkdir -p gpurun_out/final
-R=r2
+R=${R:-r2}
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/final/smi.txt 2>&1
 lscpu > gpurun_out/final/lscpu.txt 2>&1
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/final/smoke.log 2>&1
