@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(256) k_jacobi_lower(SellDev L, const T* __rest
 
 // x_new = D^-1 (b - (U - D) x)  (U off-diagonal part in SELL, D separate)
 template <typename T, bool HINT, bool D16, bool UNI>
-__global__ void __launch_bounds__(256, 8) k_jacobi_upper(SellDev U, const T* __restrict__ uval,
+__global__ void __launch_bounds__(256) k_jacobi_upper(SellDev U, const T* __restrict__ uval,
                                                       const T* __restrict__ diag,
                                                       const T* __restrict__ b,
                                                       const T* __restrict__ x,
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(256, 8) k_jacobi_upper(SellDev U, const T* __r
 // last L sweep fused with the first U iterate: writes both the L result F
 // and y1 = F / diag (saves one pass over the vectors)
 template <typename T, bool HINT, bool D16, bool UNI>
-__global__ void __launch_bounds__(256, 8) k_jacobi_lower_diag(SellDev L, const T* __restrict__ lval,
+__global__ void __launch_bounds__(256) k_jacobi_lower_diag(SellDev L, const T* __restrict__ lval,
                                                            const T* __restrict__ b,
                                                            const T* __restrict__ x,
                                                            T* __restrict__ xn,
