@@ -569,13 +569,11 @@ struct FactorBuf {
   bool on = false;
   DBuf<int32_t> sn_s, sn_r, col_ptr, col_ids, row_ptr, row_ids, in_ptr, in_idx, out_ptr, out_idx;
   DBuf<int64_t> d_off, m_off, n_off;
-  DBuf<int2> tasks, df_tasks;             // per-level launches / the dataflow order
+  DBuf<int2> df_tasks;                    // tiles in dependency order
   DBuf<int32_t> parent, child_ptr, child_idx, fwd_need, bwd_need, ready;
   DBuf<unsigned> ticket;
   int32_t n_fwd_tasks = 0, n_df_tasks = 0, n_sn = 0, df_grid = 0;
   size_t df_smem = 0;
-  std::vector<int32_t> fwd_ptr, bwd_ptr;  // per level: task ranges (forward, backward)
-  std::vector<size_t> fwd_smem, bwd_smem;
   DBuf<char> vals, ybuf, cbuf, fcm;
   DBuf<int64_t> f_off;
   DBuf<int32_t> cm_list;
@@ -867,34 +865,16 @@ T* levelset_solve(gdsw_precond* m, const double* r, cudaStream_t s) {
   return y;
 }
 
-// x = A^-1 u by a supernodal partitioned inverse: one launch per tree level
-// forward (leaves first), then one per level backward (root first)
+// x = A^-1 u by a supernodal partitioned inverse: one persistent dataflow launch
+// (both triangles, every supernode, tiles ordered leaves-first then root-first)
 template <typename T, typename TI>
 void factor_solve(const FactorBuf& F, const TI* u, const int32_t* gmap, T* x, cudaStream_t s) {
   const CoarseFactorDev D = F.dev();
-  static const bool levels = env_flag("GDSW_CF_LEVELS");
-  if (!levels) {
-    // one launch: dependency-driven tiles (k_cf_dataflow)
-    CfSched S{F.ticket.p, F.ready.p, F.ready.p + F.n_sn, F.n_fwd_tasks, F.n_df_tasks, F.n_sn};
-    k_cf_dataflow<T, TI><<<F.df_grid, CF_THREADS, F.df_smem, s>>>(D, S, F.df_tasks.p, (const T*)F.vals.p, u,
-                                                                   gmap, (T*)F.ybuf.p, (T*)F.cbuf.p, x,
-                                                                   (const T*)F.fcm.p);
-    CK_LAUNCH();
-    return;
-  }
-  const int nl = (int)F.fwd_smem.size();
-  for (int l = 0; l < nl; ++l) {
-    const int32_t t0 = F.fwd_ptr[l], nt = F.fwd_ptr[l + 1] - t0;
-    k_cf_forward<T, TI><<<nt, CF_THREADS, F.fwd_smem[l], s>>>(D, F.tasks.p + t0, (const T*)F.vals.p, u, gmap,
-                                                             (T*)F.ybuf.p, (T*)F.cbuf.p);
-    CK_LAUNCH();
-  }
-  for (int l = nl - 1; l >= 0; --l) {
-    const int32_t t0 = F.bwd_ptr[l], nt = F.bwd_ptr[l + 1] - t0;
-    k_cf_backward<T><<<nt, CF_THREADS, F.bwd_smem[l], s>>>(D, F.tasks.p + t0, (const T*)F.vals.p,
-                                                          (const T*)F.ybuf.p, x);
-    CK_LAUNCH();
-  }
+  // one launch: dependency-driven tiles (k_cf_dataflow)
+  CfSched S{F.ticket.p, F.ready.p, F.ready.p + F.n_sn, F.n_fwd_tasks, F.n_df_tasks, F.n_sn};
+  k_cf_dataflow<T, TI><<<F.df_grid, CF_THREADS, F.df_smem, s>>>(D, S, F.df_tasks.p, (const T*)F.vals.p, u, gmap,
+                                                                 (T*)F.ybuf.p, (T*)F.cbuf.p, x, (const T*)F.fcm.p);
+  CK_LAUNCH();
 }
 
 template <typename T>
@@ -929,7 +909,7 @@ T* local_solve(gdsw_precond* m, const double* r, int jacobi_iters, cudaStream_t 
 }
 
 // v = A0^-1 u: dense inverse GEMV, or the factored partitioned inverse
-// (one launch per tree level and direction)
+// (one persistent dataflow launch)
 template <typename T>
 void coarse_solve(gdsw_precond* m, cudaStream_t cs) {
   CoarsePlan* Cp = m->cp.get();
@@ -1590,50 +1570,27 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
     F.n_cm = (int32_t)cm.size();
     F.fcm.alloc((size_t)std::max<int64_t>(tot, 1) * es);
   }
-  std::vector<int2> tasks;
-  F.fwd_ptr.assign(1, 0);
-  F.fwd_smem.assign(nl, 0);
-  F.bwd_smem.assign(nl, 0);
+  // algorithmic bytes and the largest staged vector (forward: s values,
+  // backward: s + r)
   int64_t bytes = 0;
-  for (int l = 0; l < nl; ++l) {
-    for (int64_t k = f->level_ptr[l]; k < f->level_ptr[l + 1]; ++k) {
-      const int64_t s = f->sn_s[k], r = f->sn_r[k];
-      for (int64_t q = 0; q < s + r; q += CF_ROWS) tasks.push_back(make_int2((int)k, (int)q));
-      F.fwd_smem[l] = std::max(F.fwd_smem[l], (size_t)s * es);
-      bytes += (s * (s - 1) / 2 + r * s) * (int64_t)es;
-    }
-    F.fwd_ptr.push_back((int32_t)tasks.size());
-  }
-  F.bwd_ptr.assign(1, (int32_t)tasks.size());
-  for (int l = 0; l < nl; ++l) {
-    for (int64_t k = f->level_ptr[l]; k < f->level_ptr[l + 1]; ++k) {
-      const int64_t s = f->sn_s[k], r = f->sn_r[k];
-      for (int64_t q = 0; q < s; q += CF_ROWS) tasks.push_back(make_int2((int)k, (int)q));
-      F.bwd_smem[l] = std::max(F.bwd_smem[l], (size_t)(s + r) * es);
-      bytes += (s * (s + 1) / 2 + r * s) * (int64_t)es;
-    }
-    F.bwd_ptr.push_back((int32_t)tasks.size());
-  }
   size_t smax = 0;
-  for (int l = 0; l < nl; ++l) smax = std::max({smax, F.fwd_smem[l], F.bwd_smem[l]});
+  for (int k = 0; k < nsn; ++k) {
+    const int64_t s = f->sn_s[k], r = f->sn_r[k];
+    bytes += (s * s + 2 * r * s) * (int64_t)es;
+    smax = std::max(smax, (size_t)(s + r) * es);
+  }
   require(smax <= 200 * 1024, "partitioned-inverse supernode too large for shared memory");
-  F.tasks.upload(tasks);
   if (smax > 48 * 1024) {  // before the occupancy query below
     auto big = [&](auto kern) { CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax)); };
-    big(k_cf_forward<double, double>);
-    big(k_cf_forward<float, double>);
-    big(k_cf_forward<float, float>);
-    big(k_cf_backward<double>);
-    big(k_cf_backward<float>);
     big(k_cf_dataflow<double, double>);
     big(k_cf_dataflow<float, double>);
     big(k_cf_dataflow<float, float>);
   }
   // dataflow schedule: forward tiles leaves-first, backward tiles root-first;
   // parent = supernode of the first row below, readiness targets in tiles.
-  // Tile rows per level and direction: about two tiles per resident CTA
-  // slot (C3's 512 blocks: large tiles, few per-task overheads; a coarse
-  // level of one supernode: 8-row tiles over the whole GPU)
+  // Tile rows per level and direction: about one tile per resident CTA
+  // slot (GDSW_CF_TPS; measured 1 < 2 < 4 with the column-major panels: C3-
+  // sized blocks 0.28 / 0.30 / 0.40 ms), clamped to 8..128 rows
   {
     int occ = 0;
     if (dtype == GDSW_F32)
@@ -1650,7 +1607,7 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
       }
       static const int64_t tps = [] {
         const char* e = std::getenv("GDSW_CF_TPS");
-        return e ? std::max<int64_t>(1, std::atoi(e)) : (int64_t)2;
+        return e ? std::max<int64_t>(1, std::atoi(e)) : (int64_t)1;
       }();
       auto pick = [&](int64_t rows) {
         int64_t t = (rows + tps * slots - 1) / (tps * slots);
@@ -1711,7 +1668,7 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
     F.df_smem = smax;
   }
   F.bytes = bytes;
-  F.n_launch = 2 * nl;
+  F.n_launch = 1;
   with_dtype(dtype, [&](auto tag) {
     using T = decltype(tag);
     if (f->values) {
