@@ -87,11 +87,13 @@ def interface_basis(nullspace: np.ndarray, structure: InterfaceStructure) -> Int
     return InterfaceBasis(blocks, kept, z.shape[1], coeffs)
 
 
-def interior_sets(part: Partition, structure: InterfaceStructure) -> list:
-    """I_s = dofs owned by s and not on the interface (schwarz.py:177-181)."""
+def interior_sets(part: Partition, structure: InterfaceStructure, subdomains=None) -> list:
+    """I_s = dofs owned by s and not on the interface (schwarz.py:177-181);
+    `subdomains`: only those, in that order (sharded setups)."""
     on_iface = np.zeros(structure.n, dtype=bool)
     on_iface[structure.interface] = True
-    return [np.flatnonzero((part.owner == s) & ~on_iface) for s in range(part.n_parts)]
+    subs = range(part.n_parts) if subdomains is None else subdomains
+    return [np.flatnonzero((part.owner == s) & ~on_iface) for s in subs]
 
 
 def coarse_columns(structure: InterfaceStructure, basis: InterfaceBasis):

@@ -95,24 +95,54 @@ def plan_shards(a: CsrMatrix, dec, nranks: int) -> list:
             lo, hi = min(lo, int(cols.min())), max(hi, int(cols.max()) + 1)
         own.append((g0, g1))
         ext.append((lo, hi))
-    shards = []
-    for r in range(nranks):
-        (g0, g1), (e0, e1) = own[r], ext[r]
-        nbrs = []
-        for q in range(nranks):
-            if q == r:
-                continue
-            (q0, q1), (f0, f1) = own[q], ext[q]
-            recv = (max(e0, q0), min(e1, q1))   # rows q owns in my halo
-            send = (max(g0, f0), min(g1, f1))   # rows I own in q's halo
-            if recv[1] > recv[0] or send[1] > send[0]:
-                if send[1] <= send[0]:
-                    send = (g0, g0)
-                if recv[1] <= recv[0]:
-                    recv = (e0, e0)
-                nbrs.append((q, send[0] - e0, send[1] - e0, recv[0] - e0, recv[1] - e0))
-        shards.append(Shard(r, nranks, a.nrows, g0, g1, e0, e1, subs_by_rank[r], nbrs))
-    return shards
+    return [Shard(r, nranks, a.nrows, own[r][0], own[r][1], ext[r][0], ext[r][1], subs_by_rank[r],
+                  _neighbours(r, own, ext)) for r in range(nranks)]
+
+
+def _neighbours(r: int, own: list, ext: list) -> list:
+    """Halo exchange ranges of rank r from every rank's owned / extended row
+    ranges (one global numbering): (q, send_lo, send_hi, recv_lo, recv_hi)
+    relative to r's extended start."""
+    (g0, g1), (e0, e1) = own[r], ext[r]
+    nbrs = []
+    for q in range(len(own)):
+        if q == r:
+            continue
+        (q0, q1), (f0, f1) = own[q], ext[q]
+        recv = (max(e0, q0), min(e1, q1))   # rows q owns in my halo
+        send = (max(g0, f0), min(g1, f1))   # rows I own in q's halo
+        if recv[1] > recv[0] or send[1] > send[0]:
+            if send[1] <= send[0]:
+                send = (g0, g0)
+            if recv[1] <= recv[0]:
+                recv = (e0, e0)
+            nbrs.append((q, send[0] - e0, send[1] - e0, recv[0] - e0, recv[1] - e0))
+    return nbrs
+
+
+def plan_slab_shard(sp, nranks: int, rank: int, gather=None) -> Shard:
+    """This rank's layout from its slab problem (slab.py), in the window's
+    numbering; the neighbour ranges come from every rank's (global) row
+    ranges, exchanged by `gather` (default: all_gather_object)."""
+    a, sets = sp.a, sp.dec.overlap.sets
+    g0, g1 = sp.g0, sp.g1
+    lo = min([g0] + [int(sets[s][0]) for s in sp.subs])
+    hi = max([g1] + [int(sets[s][-1]) + 1 for s in sp.subs])
+    cols = a.col_idx[a.row_ptr[g0]:a.row_ptr[g1]]
+    if cols.size:
+        lo, hi = min(lo, int(cols.min())), max(hi, int(cols.max()) + 1)
+    mine = (g0 + sp.offset, g1 + sp.offset, lo + sp.offset, hi + sp.offset)
+    if gather is None and nranks > 1:
+        import torch.distributed as tdist
+
+        def gather(x):
+            out = [None] * nranks
+            tdist.all_gather_object(out, x)
+            return out
+    allr = gather(mine) if gather is not None else [mine]
+    own = [(t[0], t[1]) for t in allr]
+    ext = [(t[2], t[3]) for t in allr]
+    return Shard(rank, nranks, a.nrows, g0, g1, lo, hi, np.asarray(sp.subs), _neighbours(rank, own, ext))
 
 
 def _range_rows(lo, hi):
@@ -122,7 +152,12 @@ def _range_rows(lo, hi):
 class DistPreconditioner:
     """This rank's share of the two-level preconditioner on the GPU."""
 
-    def __init__(self, a: CsrMatrix, dec, config, nullspace, shard: Shard, pg_group=None):
+    def __init__(self, a: CsrMatrix, dec, config, nullspace, shard: Shard, pg_group=None,
+                 slab=None):
+        """`slab` (slab.SlabProblem): a, dec, nullspace and shard are the
+        rank's window (window numbering); coarse columns and the residual
+        check scales are global (the slab's column ids, max-reductions)."""
+        self.slab = slab
         import torch.distributed as tdist
 
         from . import device
@@ -208,12 +243,22 @@ class DistPreconditioner:
         if not column_map:
             raise ValueError("coarse space is empty; use use_coarse=False")
         n_c = len(column_map)
+        if self.slab is not None:
+            # the window's components carry their GLOBAL coarse columns (one
+            # per component: scalar null space)
+            if any(len(k) != 1 for k in basis.kept):
+                raise ValueError("slab setup supports one null-space column per component")
+            col = np.asarray(self.slab.comp_col, dtype=np.int64)
+            if np.any(col < 0):
+                raise ValueError("slab setup: a window component has no global coarse column")
+            n_c = int(self.slab.n_c)
+            pg = CsrMatrix(pg.nrows, n_c, pg.row_ptr, col[pg.col_idx], pg.values)
         gamma = structure.interface
         mine = (gamma >= sh.g0) & (gamma < sh.g1)
         in_ext = (gamma >= sh.e0) & (gamma < sh.e1)
         pg_rows = np.flatnonzero(mine)
         pg_own = extract_submatrix(pg, pg_rows, np.arange(pg.ncols))
-        isets = [interior_sets(dec.partition, structure)[s] - sh.e0 for s in sh.subs]
+        isets = [d - sh.e0 for d in interior_sets(dec.partition, structure, sh.subs)]
         g_own = gamma[mine] - sh.e0
         g_ext = gamma[in_ext] - sh.e0
         for d in isets:   # interiors only couple to interface rows this rank owns
@@ -230,7 +275,14 @@ class DistPreconditioner:
         np.add.at(rs, a.row_ids(), np.abs(coarse_src.values))
         gnorm = np.zeros(n_c)
         np.maximum.at(gnorm, pg.col_idx, np.abs(pg.values))
-        bad = np.flatnonzero(resid > 1e-10 * rs.max() * np.maximum(gnorm, 1e-300))
+        rs_max = rs.max()
+        if self.slab is not None and sh.nranks > 1:
+            import torch
+            import torch.distributed as tdist
+            red = torch.from_numpy(np.concatenate([[rs_max], gnorm]))
+            tdist.all_reduce(red, op=tdist.ReduceOp.MAX, group=group)
+            rs_max, gnorm = float(red[0]), red[1:].numpy()
+        bad = np.flatnonzero(resid > 1e-10 * rs_max * np.maximum(gnorm, 1e-300))
         if bad.size:
             raise ArithmeticError(
                 f"energy-minimizing extension failed the residual check for column "
@@ -293,5 +345,5 @@ def build_sharded_problem(n_xy: int, n_z_per_rank: int, boxes_xy: int, boxes_z_p
     return prob, Decomposition(part, overlap, structure)
 
 
-__all__ = ["Shard", "plan_shards", "slab_subdomains", "DistPreconditioner",
+__all__ = ["Shard", "plan_shards", "plan_slab_shard", "slab_subdomains", "DistPreconditioner",
            "build_sharded_problem", "_host"]

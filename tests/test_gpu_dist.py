@@ -121,3 +121,72 @@ def test_sharded_gmres_two_ranks_one_gpu(method):
         assert np.abs(r[9] - a0.to_dense()).max() <= 1e-12 * np.abs(a0.to_dense()).max()
     assert np.array_equal(res[0][9], res[1][9])
     assert np.linalg.norm(b - prob.a @ xs) <= 1e-7 * np.linalg.norm(b) * 1.0001
+
+
+def _slab_rank_main(rank, world, port, method, q):
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2304_04876_b200.dist import DistPreconditioner, plan_slab_shard
+    from paper_2304_04876_b200.krylov import KrylovConfig
+    from paper_2304_04876_b200.local_solvers import SolverSpec
+    from paper_2304_04876_b200.schwarz import SchwarzConfig
+    from paper_2304_04876_b200.slab import build_slab_problem
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sp = build_slab_problem(14, 8, 2, 2, world, rank)
+        sh = plan_slab_shard(sp, world, rank)
+        cfg = SchwarzConfig(local=SolverSpec(method, 0, 3, 5), ordering="natural")
+        pre = DistPreconditioner(sp.a, sp.dec, cfg, sp.nullspace, sh, slab=sp)
+        x_star = np.random.default_rng(0).standard_normal(sp.n_global)
+        b = sp.a @ x_star[sp.offset:sp.offset + sp.a.nrows]
+        bo = torch.from_numpy(b[sh.g0:sh.g1].copy()).cuda()
+        x, rep = pre.solve(bo, KrylovConfig(variant="single_reduce"))
+        torch.cuda.synchronize()
+        q.put((rank, x.cpu().numpy(), rep["iterations"], rep["converged"], list(rep["history"]),
+               pre.a0.to_dense().astype(np.float64), sp.a.nrows, sp.n_global))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("method", ["fast_ilu", "exact_lu"])
+def test_sharded_gmres_slab_setup_two_ranks(method):
+    """Every rank builds only its z-window (slab.py) -- the sharded solve
+    still equals the single-GPU solve of the global system: iterations,
+    residual history, solution, and the coarse matrix A0 (global columns)."""
+    import torch.multiprocessing as mp
+
+    from paper_2304_04876_b200.decomposition import decompose
+    from paper_2304_04876_b200.krylov import KrylovConfig, gmres
+    from paper_2304_04876_b200.schwarz import setup_numeric, setup_symbolic
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_rank_main, args=(r, world, port, method, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        res = sorted([q.get(timeout=600) for _ in procs], key=lambda t: t[0])
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    prob, dec, cfg = _problem(world, method)
+    skel = setup_symbolic(prob.a, decompose(prob.a, dec.partition, 1, "rgdsw"), cfg)
+    pre = setup_numeric(skel, prob.a, prob.nullspace)
+    b = prob.a @ np.random.default_rng(0).standard_normal(prob.a.nrows)
+    x1, rep1 = gmres(prob.a, pre, b, KrylovConfig(variant="single_reduce"))
+    assert all(r[7] == prob.a.nrows for r in res)
+    assert all(r[3] for r in res)
+    assert res[0][2] == res[1][2] and abs(res[0][2] - rep1.iterations) <= 1
+    assert np.allclose(res[0][4][:5], rep1.residual_history[:5], rtol=1e-8)
+    xs = np.concatenate([r[1] for r in res])
+    assert np.abs(xs - x1).max() <= 1e-6 * np.abs(x1).max()
+    a0 = pre.coarse.a0.to_dense()
+    for r in res:
+        assert np.abs(r[5] - a0).max() <= 1e-12 * np.abs(a0).max()
