@@ -17,14 +17,17 @@ FastSpTRSV(5 iterates) local solves, natural ordering, fp64.
   time (CUDA events recorded by libgdsw on the launching stream during the
   timed region) against MEASURED_PEAKS.json hbm_gbs.
 * cpu_baseline: the oracle (plain-C restatement of the reference's
-  sequential kernels + numpy GMRES) on a bounded sample of the same solve.
+  sequential kernels + numpy GMRES): one full solve on 1 core.
 
---impl reference: the reference's CPU path (the oracle port, entirely on the
-host, its own exact-LU coarse basis) on the same workload, bounded samples.
-Multi-GPU (torchrun, weak scaling): ONE global system of N x 2M dof
-(128 x 128 x 128N grid, 4 x 4 x 4N boxes) sharded in z-slabs, 64 subdomains
-per GPU; halos, the coarse right-hand side and the GMRES block go through
-libgdsw's peer-memory collectives (paper_2304_04876_b200.dist).
+--impl reference: the reference's CPU path (the oracle port with the
+reference's setup restated in oracle/reference_setup.py, entirely on the
+host) on the same workload: full solves on every host thread.
+Multi-GPU (--gpus N self-launches torchrun; weak scaling): ONE global system
+of N x 2M dof (128 x 128 x 128N grid, 4 x 4 x 4N boxes) sharded in z-slabs,
+64 subdomains per GPU, every rank building only its own z-window
+(paper_2304_04876_b200.slab); halos, the coarse right-hand side and the
+GMRES block go through libgdsw's peer-memory collectives
+(paper_2304_04876_b200.dist).
 """
 
 from __future__ import annotations
