@@ -127,6 +127,23 @@ __global__ void k_pinv_fcm(CoarseFactorDev F, const int32_t* __restrict__ sn_lis
   }
 }
 
+// one thread's share of a column-major panel row: columns [c, c1) of the
+// row at pc (column stride `ld`), CF_CMU loads in flight, four partial sums
+#ifndef CF_CMU
+#define CF_CMU 4
+#endif
+template <typename T>
+__device__ __forceinline__ void cm_dot(const T* __restrict__ pc, int64_t ld, int c, int c1, const T* buf, T (&a)[4]) {
+  for (; c + CF_CMU <= c1; c += CF_CMU) {
+    T v[CF_CMU];
+#pragma unroll
+    for (int uu = 0; uu < CF_CMU; ++uu) v[uu] = ldg_stream(pc + (int64_t)(c + uu) * ld);
+#pragma unroll
+    for (int uu = 0; uu < CF_CMU; ++uu) a[uu & 3] = fma(v[uu], buf[c + uu], a[uu & 3]);
+  }
+  for (; c < c1; ++c) a[0] = fma(ldg_stream(pc + (int64_t)c * ld), buf[c], a[0]);
+}
+
 template <typename T, typename TI>
 __global__ void __launch_bounds__(CF_THREADS) k_cf_dataflow(CoarseFactorDev F, CfSched S,
                                                             const int2* __restrict__ tasks,
@@ -205,14 +222,7 @@ __global__ void __launch_bounds__(CF_THREADS) k_cf_dataflow(CoarseFactorDev F, C
         if (on) {
           const T* pc = P + row;
           int c = c0;
-          for (; c + 4 <= c1; c += 4) {
-            T v[4];
-#pragma unroll
-            for (int uu = 0; uu < 4; ++uu) v[uu] = ldg_stream(pc + (int64_t)(c + uu) * (s + r));
-#pragma unroll
-            for (int uu = 0; uu < 4; ++uu) a[uu] = fma(v[uu], buf[c + uu], a[uu]);
-          }
-          for (; c < c1; ++c) a[0] = fma(ldg_stream(pc + (int64_t)c * (s + r)), buf[c], a[0]);
+          cm_dot(pc, (int64_t)(s + r), c, c1, buf, a);
         }
         red[threadIdx.x] = (a[0] + a[1]) + (a[2] + a[3]);
         __syncthreads();
@@ -265,14 +275,7 @@ __global__ void __launch_bounds__(CF_THREADS) k_cf_dataflow(CoarseFactorDev F, C
         if (on) {
           const T* pc = P + row;
           int c = c0;
-          for (; c + 4 <= c1; c += 4) {
-            T v[4];
-#pragma unroll
-            for (int uu = 0; uu < 4; ++uu) v[uu] = ldg_stream(pc + (int64_t)(c + uu) * s);
-#pragma unroll
-            for (int uu = 0; uu < 4; ++uu) a[uu] = fma(v[uu], buf[c + uu], a[uu]);
-          }
-          for (; c < c1; ++c) a[0] = fma(ldg_stream(pc + (int64_t)c * s), buf[c], a[0]);
+          cm_dot(pc, (int64_t)s, c, c1, buf, a);
         }
         red[threadIdx.x] = (a[0] + a[1]) + (a[2] + a[3]);
         __syncthreads();
