@@ -2,10 +2,18 @@
 // stream around each phase while enabled, resolved lazily on read. Used by
 // bench.py for the per-kernel roofline (launch duration from events on the
 // kernel's own stream, never from a profiler).
+//
+// NVTX: with GDSW_NVTX=1 every phase is also an NVTX range named after its
+// kernel (header-only nvtx3; ranges appear in Nsight Systems / ncu
+// --nvtx-include filters; eager launches only -- a replayed CUDA graph has no
+// host-side ranges).
 #pragma once
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "common.cuh"
 
@@ -59,13 +67,26 @@ inline Prof& prof() {
 }
 
 // RAII scope: records start/stop events on `stream` when profiling is on
+inline bool nvtx_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("GDSW_NVTX");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 struct ProfScope {
   int k = -1;
   cudaStream_t s;
   cudaEvent_t e0 = nullptr;
   double bytes;
+  bool nvtx = false;
   ProfScope(const char* name, cudaStream_t stream, double algorithmic_bytes)
       : s(stream), bytes(algorithmic_bytes) {
+    if (nvtx_on()) {
+      nvtxRangePushA(name);
+      nvtx = true;
+    }
     Prof& P = prof();
     if (!P.on) return;
     std::lock_guard<std::mutex> g(P.mu);
@@ -74,6 +95,7 @@ struct ProfScope {
     CK(cudaEventRecord(e0, s));
   }
   ~ProfScope() {
+    if (nvtx) nvtxRangePop();
     if (k < 0) return;
     Prof& P = prof();
     std::lock_guard<std::mutex> g(P.mu);
