@@ -44,6 +44,35 @@ __device__ __forceinline__ void sr_coef_compute(int j, const double* blk, double
 }
 
 
+
+// the last CTA to finish reduces all per-CTA partials in CTA order
+// (deterministic) and, for a single-reduce block, computes the next update's
+// scalars (k_sr_coef folded in); the ticket resets itself
+__device__ __forceinline__ void block_dot_finish(int nv, int nrc, int nslots, double* __restrict__ partial,
+                                                 double* __restrict__ out, unsigned* __restrict__ counter,
+                                                 double* __restrict__ coef) {
+  constexpr int NW = KDOT_THREADS / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int k = warp; k < 2 * nrc; k += NW) {
+    double s = 0.0;
+    for (int b = lane; b < nslots; b += 32) s += __ldcg(partial + (int64_t)b * KDOT_W2 + k);
+    s = warp_sum(s);
+    if (lane == 0) out[k] = s;
+  }
+  if (coef) {
+    __syncthreads();
+    if (threadIdx.x == 0) sr_coef_compute(nv, out, coef);
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
 // rows of the combined list [V[0..nv), v] restricted to [r0, r0 + nrc),
 // nrc <= NR. out[2*rr + {0,1}] = row . v, row . z  (rr = local row index).
 // Each thread owns element pairs (grid-stride, 16-byte loads) and keeps
@@ -197,43 +226,143 @@ __global__ void __launch_bounds__(KDOT_THREADS, NR > 8 ? 1 : 2) k_block_dot(
     for (int w = 0; w < NW; ++w) a += red[w][k];
     partial[(int64_t)blockIdx.x * KDOT_W2 + k] = a;
   }
-  // the last CTA reduces all per-CTA partials in a fixed order
-  __shared__ bool last;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  for (int k = warp; k < 2 * nrc; k += NW) {
-    double s = 0.0;
-    for (int b = lane; b < (int)gridDim.x; b += 32) s += __ldcg(partial + (int64_t)b * KDOT_W2 + k);
-    s = warp_sum(s);
-    if (lane == 0) out[k] = s;
-  }
-  if (coef) {
-    // the whole block is in: the next update's scalars (k_sr_coef) here
-    __syncthreads();
-    if (threadIdx.x == 0) sr_coef_compute(nv, out, coef);
-  }
-  if (threadIdx.x == 0) *counter = 0u;
+  block_dot_finish(nv, nrc, (int)gridDim.x, partial, out, counter, coef);
 }
 
-// host dispatch on the row-count bucket
-inline void launch_block_dot(unsigned grid, cudaStream_t s, int64_t n, const double* V, int64_t ldv,
+// Row-group block dot (the 16-byte path for 5+ rows): the rows are cut into
+// groups of KRG, CTA b works on group b % ng and grid-strides the element
+// pairs with the other CTAs of its group, holding only 2*KRG running sums.
+// That keeps four CTAs (32 warps) resident per SM; v and z are re-read once
+// per group, from L2 (the groups' CTAs sweep the same pairs together). The
+// grid is one full wave (KRG_CTAS_PER_SM x SMs, split evenly over the groups):
+// a partial second wave costs up to 20% (tools/micro/bench_blockdot3.cu).
+// Per-CTA partials sit in the CTA's slot at the group's row offset; the last
+// CTA sums the slots in order (deterministic).
+constexpr int KRG = 4;
+constexpr int KRG_CTAS_PER_SM = 4;
+
+// HZ: z present (a compile-time switch: a run-time one splits the load batch)
+template <bool HZ>
+__global__ void __launch_bounds__(KDOT_THREADS, KRG_CTAS_PER_SM) k_block_dot_rg(
+    int64_t n, const double* __restrict__ V, int64_t ldv, int nv, int r0, int nrc,
+    const double* __restrict__ v, const double* __restrict__ z, double* __restrict__ partial,
+    double* __restrict__ out, unsigned* __restrict__ counter, double* __restrict__ coef) {
+  constexpr int NW = KDOT_THREADS / 32;
+  __shared__ double red[NW][2 * KRG];
+  const int ng = (nrc + KRG - 1) / KRG;
+  const int g = blockIdx.x % ng, cta = blockIdx.x / ng, ncta = gridDim.x / ng;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q0 = g * KRG;
+  const int nr = min(KRG, nrc - q0);                // rows of this group
+  const int nb = max(0, min(nr, nv - r0 - q0));     // basis rows among them
+  const bool self = nv - r0 - q0 >= 0 && nv - r0 - q0 < nr;
+  constexpr bool hz = HZ;
+  double av[KRG], az[KRG], as = 0.0, zs = 0.0;
+#pragma unroll
+  for (int q = 0; q < KRG; ++q) av[q] = az[q] = 0.0;
+  if (cta < ncta) {  // gridDim.x is a multiple of ng; guard anyway
+    const int64_t n2 = n >> 1, ld2 = ldv >> 1;
+    const int64_t nth = (int64_t)ncta * KDOT_THREADS;
+    // slots past the group's basis rows read v (cached, ignored): every
+    // load of a step is then unconditional and issued back to back
+    const double2* rp[KRG];
+#pragma unroll
+    for (int u = 0; u < KRG; ++u)
+      rp[u] = u < nb ? reinterpret_cast<const double2*>(V + (int64_t)(r0 + q0 + u) * ldv)
+                     : reinterpret_cast<const double2*>(v);
+    (void)ld2;
+#pragma unroll 1
+    for (int64_t i = (int64_t)cta * KDOT_THREADS + threadIdx.x; i < n2; i += nth) {
+      double2 x[KRG];
+#pragma unroll
+      for (int u = 0; u < KRG; ++u) x[u] = ldg_stream(rp[u] + i);
+      const double2 pv = __ldg(reinterpret_cast<const double2*>(v) + i);
+      const double2 pz = hz ? __ldg(reinterpret_cast<const double2*>(z) + i) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < KRG; ++u)
+        if (u < nb) {
+          av[u] = fma(x[u].y, pv.y, fma(x[u].x, pv.x, av[u]));
+          az[u] = fma(x[u].y, pz.y, fma(x[u].x, pz.x, az[u]));
+        }
+      if (self) {
+        as = fma(pv.y, pv.y, fma(pv.x, pv.x, as));
+        zs = fma(pv.y, pz.y, fma(pv.x, pz.x, zs));
+      }
+    }
+    if ((n & 1) && cta == 0 && threadIdx.x == 0) {
+      const int64_t e = n - 1;
+      const double ve = v[e], ze = hz ? z[e] : 0.0;
+      const double* pe = V + (int64_t)(r0 + q0) * ldv + e;
+#pragma unroll
+      for (int q = 0; q < KRG; ++q) {
+        if (q < nb) {
+          av[q] = fma(*pe, ve, av[q]);
+          az[q] = fma(*pe, ze, az[q]);
+        }
+        pe += ldv;
+      }
+      as = fma(ve, ve, as);
+      zs = fma(ve, ze, zs);
+    }
+  }
+  if (self) {  // the self row sits at slot nb
+#pragma unroll
+    for (int q = 0; q < KRG; ++q)
+      if (q == nb) {
+        av[q] = as;
+        az[q] = zs;
+      }
+  }
+#pragma unroll
+  for (int q = 0; q < KRG; ++q) {
+    if (q < nr) {
+      const double a = warp_sum(av[q]);
+      const double c = warp_sum(az[q]);
+      if (lane == 0) {
+        red[warp][2 * q] = a;
+        red[warp][2 * q + 1] = c;
+      }
+    }
+  }
+  __syncthreads();
+  if (cta < ncta)
+    for (int k = threadIdx.x; k < 2 * nr; k += KDOT_THREADS) {
+      double a = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w) a += red[w][k];
+      partial[(int64_t)cta * KDOT_W2 + 2 * q0 + k] = a;
+    }
+  block_dot_finish(nv, nrc, ncta, partial, out, counter, coef);
+}
+
+// partial slots a block dot may use on `sms` SMs
+inline int block_dot_slots(int sms) { return KRG_CTAS_PER_SM * sms; }
+
+// host dispatch: the row-group kernel on the 16-byte path from 5 rows up,
+// the all-rows-per-thread kernel for 1-4 rows (equal there) and for the
+// unaligned path
+inline void launch_block_dot(int sms, cudaStream_t s, int64_t n, const double* V, int64_t ldv,
                              int nv, int r0, int nrc, const double* v, const double* z,
                              double* partial, double* out, unsigned* counter, double* coef = nullptr) {
-  // EP = 2 (two element pairs per step) measured 5-20% faster for the 4- and
-  // 16-row buckets and neutral / slower for 8 (tools/micro/bench_blockdot2.cu)
-  if (nrc <= 4)
+  const bool vec = ((ldv & 1) == 0) && ((reinterpret_cast<uintptr_t>(V) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(v) & 15) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(z) & 15) == 0);
+  const unsigned grid = 2 * sms;
+  if (vec && nrc > 4 && V) {
+    const int ng = (nrc + KRG - 1) / KRG;
+    const int per = std::max(1, KRG_CTAS_PER_SM * sms / ng);
+    if (z)
+      k_block_dot_rg<true><<<per * ng, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out, counter,
+                                                            coef);
+    else
+      k_block_dot_rg<false><<<per * ng, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out, counter,
+                                                             coef);
+  } else if (nrc <= 4)
     k_block_dot<4, 2><<<grid, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out, counter, coef);
   else if (nrc <= 8)
     k_block_dot<8><<<grid, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out, counter, coef);
   else if (nrc <= 16)  // 32+ running sums: one CTA per SM (launch bound), half the grid
     k_block_dot<16, 2><<<(grid + 1) / 2, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out,
-                                                          counter, coef);
-  else if (nrc <= 24)
-    k_block_dot<24><<<(grid + 1) / 2, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out,
                                                           counter, coef);
   else
     k_block_dot<32><<<(grid + 1) / 2, KDOT_THREADS, 0, s>>>(n, V, ldv, nv, r0, nrc, v, z, partial, out,
