@@ -105,12 +105,16 @@ template <typename T>
 void spmv_T(const gdsw_csr* a, const T* x, const T* yin, T* y, int mode, double alpha, double beta,
             cudaStream_t s) {
   if (a->nrows == 0) return;
-  if (a->pat.has16)
-    k_sell_spmv<T, true><<<grid_for(a->nrows, TB), TB, 0, s>>>(a->pat.view(), (const T*)a->sell_val.p, x,
-                                                              yin, y, mode, (T)alpha, (T)beta);
+  const int f = a->pat.fmt();
+  if (f == SELL_MASK)
+    k_sell_spmv<T, SELL_MASK><<<grid_for(a->nrows, TB), TB, 0, s>>>(a->pat.view(), (const T*)a->sell_val.p, x,
+                                                                   yin, y, mode, (T)alpha, (T)beta);
+  else if (f == SELL_D16)
+    k_sell_spmv<T, SELL_D16><<<grid_for(a->nrows, TB), TB, 0, s>>>(a->pat.view(), (const T*)a->sell_val.p, x,
+                                                                  yin, y, mode, (T)alpha, (T)beta);
   else
-    k_sell_spmv<T, false><<<grid_for(a->nrows, TB), TB, 0, s>>>(a->pat.view(), (const T*)a->sell_val.p, x,
-                                                               yin, y, mode, (T)alpha, (T)beta);
+    k_sell_spmv<T, SELL_COL32><<<grid_for(a->nrows, TB), TB, 0, s>>>(a->pat.view(), (const T*)a->sell_val.p, x,
+                                                                    yin, y, mode, (T)alpha, (T)beta);
   CK_LAUNCH();
 }
 }  // namespace
@@ -154,7 +158,8 @@ int gdsw_csr_spmv(const gdsw_csr* a, const void* x, void* y, double alpha, doubl
                   void* stream) {
   return guarded([&] {
     int mode = (alpha == 1.0 && beta == 0.0) ? 0 : 2;
-    ProfScope ps("spmv", S(stream), (double)a->nnz * (esize(a->dtype) + (a->pat.has16 ? 2 : 4)) + (a->nrows + 1) * 2.0 +
+    ProfScope ps("spmv", S(stream), (double)a->nnz * (esize(a->dtype) + a->pat.idx_bytes_per_entry()) +
+                                        a->nrows * a->pat.idx_bytes_per_row() +
                                         2.0 * a->nrows * esize(a->dtype));
     with_dtype(a->dtype, [&](auto tag) {
       using T = decltype(tag);
@@ -209,8 +214,14 @@ struct gdsw_plan {
   DBuf<int32_t> res_pl, res_pu, res_tl, res_tu;
   void ensure_sell() {
     if (sell_ready) return;
-    l_sell.build(n_loc, h_l_ptr.data(), h_l_idx.data(), row_add.data(), 0);
-    u_sell.build(n_loc, h_u_ptr.data(), h_u_idx.data(), row_add.data(), 1);
+    // the sweeps take one column format for both factors: slot masks only
+    // when both patterns allow them
+    int32_t wl = 0, wu = 0;
+    const bool mk = SellPattern::mask_feasible(n_loc, h_l_ptr.data(), h_l_idx.data(), row_add.data(), 0, &wl) &&
+                    SellPattern::mask_feasible(n_loc, h_u_ptr.data(), h_u_idx.data(), row_add.data(), 1, &wu);
+    l_sell.build(n_loc, h_l_ptr.data(), h_l_idx.data(), row_add.data(), 0, mk);
+    u_sell.build(n_loc, h_u_ptr.data(), h_u_idx.data(), row_add.data(), 1, mk);
+    require(l_sell.masked == u_sell.masked, "factor layouts disagree");
     sell_ready = true;
   }
 
@@ -695,7 +706,7 @@ namespace {
 // FastSpTRSV: `iters` Jacobi iterates on L then U; returns the buffer
 // holding the block solutions
 
-template <typename T, bool HINT, bool D16, bool UNI>
+template <typename T, bool HINT, int FMT, bool UNI>
 T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   gdsw_plan* P = m->plan;
   const int32_t n = (int32_t)P->n_loc;
@@ -704,9 +715,10 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   T* X2 = (T*)m->x2.p;
   SellDev L = P->l_sell.view(), U = P->u_sell.view();
   const unsigned g = grid_for(n, TB);
-  const double cb = D16 ? 2.0 : 4.0;  // stored column bytes per entry
-  const double lbytes = (double)P->nnz_l * (sizeof(T) + cb) + n * (2.0 + 3 * sizeof(T));
-  const double ubytes = (double)(P->nnz_u - n) * (sizeof(T) + cb) + n * (2.0 + 3 * sizeof(T));
+  const double cb = P->l_sell.idx_bytes_per_entry();  // stored column bytes per entry
+  const double rb = P->l_sell.idx_bytes_per_row();    // row length / slot mask bytes
+  const double lbytes = (double)P->nnz_l * (sizeof(T) + cb) + n * (rb + 3 * sizeof(T));
+  const double ubytes = (double)(P->nnz_u - n) * (sizeof(T) + cb) + n * (rb + 3 * sizeof(T));
   // algorithmic bytes per launch: SELL values+columns once, row lengths,
   // b and x read once (gathers assumed cached), x_new written; the gather
   // variant reads r through gmap (4 + 8 per row, twice for the neighbours'
@@ -720,14 +732,14 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   } else {
     {
       ProfScope ps("gather_jacobi_lower", s, lbytes + n * (12.0 - sizeof(T)));
-      k_gather_jacobi_lower<T, HINT, D16, UNI><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, P->gmap.p, r, B, X1);
+      k_gather_jacobi_lower<T, HINT, FMT, UNI><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, P->gmap.p, r, B, X1);
       CK_LAUNCH();
     }
     T* cur = X1;
     T* oth = X2;
     for (int t = 2; t < iters - 1; ++t) {
       ProfScope ps("jacobi_lower", s, lbytes);
-      k_jacobi_lower<T, HINT, D16, UNI><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth);
+      k_jacobi_lower<T, HINT, FMT, UNI><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth);
       CK_LAUNCH();
       std::swap(cur, oth);
     }
@@ -736,7 +748,7 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
       T* X3 = (T*)m->x3.p;
       {
         ProfScope ps("jacobi_lower_diag", s, lbytes + n * 2.0 * sizeof(T));
-        k_jacobi_lower_diag<T, HINT, D16, UNI><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth,
+        k_jacobi_lower_diag<T, HINT, FMT, UNI><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth,
                                                 (const T*)m->udiag.p, X3);
         CK_LAUNCH();
       }
@@ -745,7 +757,7 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
       T* Hf = cur;  // B and cur are free now
       for (int t = 1; t < iters; ++t) {
         ProfScope ps("jacobi_upper", s, ubytes + n * (double)sizeof(T));
-        k_jacobi_upper<T, HINT, D16, UNI><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, Gf, Hf);
+        k_jacobi_upper<T, HINT, FMT, UNI><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, Gf, Hf);
         CK_LAUNCH();
         std::swap(Gf, Hf);
       }
@@ -765,7 +777,7 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   T* oth = H;
   for (int t = 1; t < iters; ++t) {
     ProfScope ps("jacobi_upper", s, ubytes + n * (double)sizeof(T));
-    k_jacobi_upper<T, HINT, D16, UNI><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, cur, oth);
+    k_jacobi_upper<T, HINT, FMT, UNI><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, cur, oth);
     CK_LAUNCH();
     std::swap(cur, oth);
   }
@@ -883,7 +895,7 @@ T* local_solve(gdsw_precond* m, const double* r, int jacobi_iters, cudaStream_t 
   if (jacobi_iters > 0 || P->method == GDSW_FAST_ILU) {
     m->ensure_jacobi();
     const int it = jacobi_iters > 0 ? jacobi_iters : m->iters;
-    const bool d16 = P->l_sell.has16 && P->u_sell.has16;
+    const int f = P->l_sell.masked ? SELL_MASK : (P->l_sell.has16 && P->u_sell.has16) ? SELL_D16 : SELL_COL32;
     // uniform-width rows (all slots loaded at once): C2 sweeps 28.0/35.2/33.9
     // -> 25.9/30.2/27.8 us (GDSW_JACOBI_UNI=0 selects the plain loop)
     static const bool uni_off = [] {
@@ -892,11 +904,17 @@ T* local_solve(gdsw_precond* m, const double* r, int jacobi_iters, cudaStream_t 
     }();
     const bool uni = !uni_off && P->l_sell.uw >= 1 && P->l_sell.uw <= 4 && P->u_sell.uw >= 1 &&
                      P->u_sell.uw <= 4;
+    if (f == SELL_MASK)
+      return uni ? jacobi_solve<T, false, SELL_MASK, true>(m, r, it, s)
+                 : jacobi_solve<T, false, SELL_MASK, false>(m, r, it, s);
     if (l2_hints_enabled())
-      return d16 ? jacobi_solve<T, true, true, false>(m, r, it, s) : jacobi_solve<T, true, false, false>(m, r, it, s);
+      return f == SELL_D16 ? jacobi_solve<T, true, SELL_D16, false>(m, r, it, s)
+                           : jacobi_solve<T, true, SELL_COL32, false>(m, r, it, s);
     if (uni)
-      return d16 ? jacobi_solve<T, false, true, true>(m, r, it, s) : jacobi_solve<T, false, false, true>(m, r, it, s);
-    return d16 ? jacobi_solve<T, false, true, false>(m, r, it, s) : jacobi_solve<T, false, false, false>(m, r, it, s);
+      return f == SELL_D16 ? jacobi_solve<T, false, SELL_D16, true>(m, r, it, s)
+                           : jacobi_solve<T, false, SELL_COL32, true>(m, r, it, s);
+    return f == SELL_D16 ? jacobi_solve<T, false, SELL_D16, false>(m, r, it, s)
+                         : jacobi_solve<T, false, SELL_COL32, false>(m, r, it, s);
   }
   if (m->lf.on) {
     // exact LU: supernodal partitioned inverses of every block
@@ -1460,12 +1478,7 @@ static void coarse_galerkin(gdsw_precond* m, const gdsw_csr* a, gdsw_dist* d, do
       }
       if (d) d->halo_fwd(z.p, 0);
       if (a->nrows > 0) {
-        if (a->pat.has16)
-          k_sell_spmv<double, true><<<grid_for(a->nrows, TB), TB>>>(a->pat.view(), aval, z.p, nullptr, y.p + off,
-                                                                   0, 1.0, 0.0);
-        else
-          k_sell_spmv<double, false><<<grid_for(a->nrows, TB), TB>>>(a->pat.view(), aval, z.p, nullptr, y.p + off,
-                                                                    0, 1.0, 0.0);
+        spmv_T<double>(a, z.p, nullptr, y.p + off, 0, 1.0, 0.0, 0);
         CK_LAUNCH();
       }
       if (Cp->n_chunks > 0) {
