@@ -146,7 +146,7 @@ def workload(args, world: int = 1, sharded: bool = False) -> dict:
 
 
 PHASE_KERNEL = {"jacobi_upper": "k_jacobi_upper", "jacobi_lower": "k_jacobi_lower",
-                "sr_update": "k_sr_update", "block_dot": "k_block_dot",
+                "sr_update": "k_sr_update", "block_dot": "k_block_dot_rg",
                 "restrict_panels": "k_restrict_chunks", "prolong": "k_prolong",
                 "spmv": "k_sell_spmv", "jacobi_fused": "k_jacobi_cluster"}
 
