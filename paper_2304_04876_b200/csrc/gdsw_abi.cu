@@ -715,6 +715,17 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   T* X2 = (T*)m->x2.p;
   SellDev L = P->l_sell.view(), U = P->u_sell.view();
   const unsigned g = grid_for(n, TB);
+  // alternate the sweeps' direction (GDSW_SWEEP_ALT=0: all forward)
+  static const bool alt = [] {
+    const char* e = std::getenv("GDSW_SWEEP_ALT");
+    return !(e && e[0] == '0');
+  }();
+  int dir = 0;
+  auto next_dir = [&] {
+    const int d = dir;
+    if (alt) dir ^= 1;
+    return d;
+  };
   const double cb = P->l_sell.idx_bytes_per_entry();  // stored column bytes per entry
   const double rb = P->l_sell.idx_bytes_per_row();    // row length / slot mask bytes
   const double lbytes = (double)P->nnz_l * (sizeof(T) + cb) + n * (rb + 3 * sizeof(T));
@@ -732,14 +743,15 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   } else {
     {
       ProfScope ps("gather_jacobi_lower", s, lbytes + n * (12.0 - sizeof(T)));
-      k_gather_jacobi_lower<T, HINT, FMT, UNI><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, P->gmap.p, r, B, X1);
+      k_gather_jacobi_lower<T, HINT, FMT, UNI><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, P->gmap.p, r, B, X1,
+                                                                   next_dir());
       CK_LAUNCH();
     }
     T* cur = X1;
     T* oth = X2;
     for (int t = 2; t < iters - 1; ++t) {
       ProfScope ps("jacobi_lower", s, lbytes);
-      k_jacobi_lower<T, HINT, FMT, UNI><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth);
+      k_jacobi_lower<T, HINT, FMT, UNI><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth, next_dir());
       CK_LAUNCH();
       std::swap(cur, oth);
     }
@@ -749,7 +761,7 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
       {
         ProfScope ps("jacobi_lower_diag", s, lbytes + n * 2.0 * sizeof(T));
         k_jacobi_lower_diag<T, HINT, FMT, UNI><<<g, TB, 0, s>>>(L, (const T*)m->lsell.p, B, cur, oth,
-                                                (const T*)m->udiag.p, X3);
+                                                (const T*)m->udiag.p, X3, next_dir());
         CK_LAUNCH();
       }
       F = oth;
@@ -757,7 +769,8 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
       T* Hf = cur;  // B and cur are free now
       for (int t = 1; t < iters; ++t) {
         ProfScope ps("jacobi_upper", s, ubytes + n * (double)sizeof(T));
-        k_jacobi_upper<T, HINT, FMT, UNI><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, Gf, Hf);
+        k_jacobi_upper<T, HINT, FMT, UNI><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, Gf, Hf,
+                                                                next_dir());
         CK_LAUNCH();
         std::swap(Gf, Hf);
       }
@@ -777,7 +790,8 @@ T* jacobi_solve(gdsw_precond* m, const double* r, int iters, cudaStream_t s) {
   T* oth = H;
   for (int t = 1; t < iters; ++t) {
     ProfScope ps("jacobi_upper", s, ubytes + n * (double)sizeof(T));
-    k_jacobi_upper<T, HINT, FMT, UNI><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, cur, oth);
+    k_jacobi_upper<T, HINT, FMT, UNI><<<g, TB, 0, s>>>(U, (const T*)m->usell.p, (const T*)m->udiag.p, F, cur, oth,
+                                                                next_dir());
     CK_LAUNCH();
     std::swap(cur, oth);
   }

@@ -388,6 +388,22 @@ struct VecIO {
   }
 };
 
+// sweep direction: rev = 1 runs the row blocks from the end, so a sweep that
+// follows one in the other direction starts on the rows whose factor values
+// and vectors the previous sweep left in L2 (the sweeps alternate)
+__device__ __forceinline__ int32_t sweep_row(int rev) {
+  const int32_t b = rev ? (int32_t)(gridDim.x - 1 - blockIdx.x) : (int32_t)blockIdx.x;
+  return b * (int32_t)blockDim.x + (int32_t)threadIdx.x;
+}
+
+// factor values of the sweeps: evict-first (streamed) measured best with the
+// alternating directions (C2 32.83 ms; default policy 33.61 ms; evict-first
+// with forward-only sweeps 33.33 ms, tools/gpu_r2c_alt.sh); the vectors keep
+// the default policy, so the next sweep's start hits them in L2
+constexpr bool SWEEP_VAL_EF = true;
+template <typename T>
+__device__ __forceinline__ T ld_fval(const T* p) { return SWEEP_VAL_EF ? ldg_stream(p) : __ldg(p); }
+
 // one Jacobi row: acc - sum_k val_k x[col_k] in column order. UNI (uniform
 // slice width <= 4): every slot's column and value are loaded at once,
 // independent of the row length, then the row's own gathers.
@@ -402,7 +418,7 @@ __device__ __forceinline__ T jac_row(const SellDev& M, const T* __restrict__ val
       if (k < M.uw) {
         const int64_t q = base + 32 * (int64_t)k;
         if constexpr (F != SELL_MASK) c[k] = sell_col<F>(M, i, q);
-        v[k] = ldg_stream(val + q);
+        v[k] = ld_fval(val + q);
       }
     }
     if constexpr (F == SELL_MASK) sell_cols<F, 4>(M, i, base, len, c);
@@ -419,7 +435,7 @@ __device__ __forceinline__ T jac_row(const SellDev& M, const T* __restrict__ val
       int32_t c;
       if constexpr (F == SELL_MASK) c = mc.next();
       else c = sell_col<F>(M, i, q);
-      acc = rn_sub(acc, rn_mul(ldg_stream(val + q), io.ld(x + c)));
+      acc = rn_sub(acc, rn_mul(ld_fval(val + q), io.ld(x + c)));
     }
   }
   return acc;
@@ -429,8 +445,8 @@ template <typename T, bool HINT, int F, bool UNI>
 __global__ void __launch_bounds__(256) k_jacobi_lower(SellDev L, const T* __restrict__ lval,
                                                       const T* __restrict__ b,
                                                       const T* __restrict__ x,
-                                                      T* __restrict__ xn) {
-  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+                                                      T* __restrict__ xn, int rev) {
+  const int32_t i = sweep_row(rev);
   if (i >= L.n_rows) return;
   const VecIO<T, HINT> io;
   const int64_t base = sell_base(L, i);
@@ -445,8 +461,8 @@ __global__ void __launch_bounds__(256) k_jacobi_upper(SellDev U, const T* __rest
                                                       const T* __restrict__ diag,
                                                       const T* __restrict__ b,
                                                       const T* __restrict__ x,
-                                                      T* __restrict__ xn) {
-  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+                                                      T* __restrict__ xn, int rev) {
+  const int32_t i = sweep_row(rev);
   if (i >= U.n_rows) return;
   const VecIO<T, HINT> io;
   const int64_t base = sell_base(U, i);
@@ -463,8 +479,8 @@ __global__ void __launch_bounds__(256) k_jacobi_lower_diag(SellDev L, const T* _
                                                            const T* __restrict__ x,
                                                            T* __restrict__ xn,
                                                            const T* __restrict__ diag,
-                                                           T* __restrict__ y1) {
-  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+                                                           T* __restrict__ y1, int rev) {
+  const int32_t i = sweep_row(rev);
   if (i >= L.n_rows) return;
   const VecIO<T, HINT> io;
   const int64_t base = sell_base(L, i);
@@ -498,8 +514,8 @@ __global__ void __launch_bounds__(256) k_gather_jacobi_lower(SellDev L,
                                                              const int32_t* __restrict__ gmap,
                                                              const double* __restrict__ r,
                                                              T* __restrict__ b,
-                                                             T* __restrict__ xn) {
-  int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+                                                             T* __restrict__ xn, int rev) {
+  const int32_t i = sweep_row(rev);
   if (i >= L.n_rows) return;
   const int64_t base = sell_base(L, i);
   const int len = sell_len<F>(L, i);
@@ -520,7 +536,7 @@ __global__ void __launch_bounds__(256) k_gather_jacobi_lower(SellDev L,
       if (UNI ? u < L.uw : k0 + u < len) {
         const int64_t q = base + 32 * (int64_t)(k0 + u);
         if constexpr (F != SELL_MASK) c[u] = sell_col<F>(L, i, q);
-        v[u] = ldg_stream(lval + q);
+        v[u] = ld_fval(lval + q);
       }
     }
     int32_t g[W];

@@ -68,6 +68,50 @@ def test_spmv_bitwise_against_oracle():
         assert np.array_equal(yy.cpu().numpy(), want - want)
 
 
+def _banded(n, offsets_of_slice, rng, p_keep):
+    """Random matrix whose rows draw their columns from a per-slice offset set
+    (ragged rows, empty rows, clipping at the matrix edges)."""
+    rows, cols = [], []
+    for i in range(n):
+        offs = offsets_of_slice(i // 32)
+        for o in sorted(offs):
+            j = i + o
+            if 0 <= j < n and rng.random() < p_keep:
+                rows.append(i)
+                cols.append(j)
+    d = np.zeros((n, n))
+    d[rows, cols] = rng.standard_normal(len(rows))
+    return CsrMatrix.from_dense(d)
+
+
+@pytest.mark.parametrize("no_mask", [False, True])
+def test_spmv_offset_mask_layout_bitwise(no_mask, monkeypatch):
+    """The offset-mask column layout (sparse.cuh SellMaskCols): slices with up
+    to eight distinct offsets, ragged and empty rows, non-uniform slice widths
+    (the sell_row chunk loop), a slice set with nine offsets (fallback to
+    per-entry columns); GDSW_NO_SELL_MASK=1 forces the per-entry layout. The
+    SpMV must be bit-identical to the oracle either way."""
+    torch = _torch()
+    from paper_2304_04876_b200.device import DeviceCsr
+    if no_mask:
+        monkeypatch.setenv("GDSW_NO_SELL_MASK", "1")
+    rng = np.random.default_rng(7)
+    base8 = [-300, -41, -7, -1, 0, 2, 33, 290]
+    mats = [
+        _banded(700, lambda s: base8, rng, 0.6),                                   # <= 8 per slice
+        _banded(700, lambda s: [o + (s % 3) for o in base8], rng, 0.9),            # slice-dependent
+        _banded(650, lambda s: base8[:3] if s % 2 else base8, rng, 0.35),          # sparse, ragged
+        _banded(500, lambda s: base8 + [97] if s == 5 else base8, rng, 0.8),       # one slice has 9
+    ]
+    for a in mats:
+        x = rng.standard_normal(a.ncols)
+        want = O.spmv(a.row_ptr, a.col_idx, a.values, x)
+        dev = DeviceCsr(a)
+        y = torch.zeros(a.nrows, dtype=torch.float64, device="cuda")
+        dev.spmv(torch.from_numpy(x).cuda(), y)
+        assert np.array_equal(y.cpu().numpy(), want)
+
+
 TS_CHAIN = 128   # tristream.cuh TR_SEG: rows up to this length keep the sequential order
 LONG_ROW_TOL = 1e-13
 
