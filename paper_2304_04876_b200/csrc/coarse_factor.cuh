@@ -19,7 +19,15 @@
 
 namespace gdsw {
 
-constexpr int CF_THREADS = 256;
+// CTA shapes of the dataflow kernel (48 registers either way): local exact-LU
+// blocks that outnumber the SMs run 128 threads x 10 resident CTAs (C3-sized
+// blocks 0.245 -> 0.220 ms, C3 92.4 -> 87.8 ms), the coarse factor and few
+// blocks 256 x 5 (128 threads measured slower there: n_c = 12,600, C5 2,048
+// subdomains 41.6 -> 44.9 ms; C1 4.4 -> 4.56 ms). A narrow
+// tile (thread per row, columns split in at least two parts) holds at most
+// NT / 2 rows: the host tiler clamps to that.
+constexpr int CF_NT_LOCAL = 128, CF_NT_COARSE = 256;
+constexpr int cf_min_ctas(int nt) { return nt == 128 ? 10 : 5; }
 constexpr int CF_ROWS = 8;   // smallest tile: one row per warp
 
 struct CoarseFactorDev {
@@ -144,11 +152,10 @@ __device__ __forceinline__ void cm_dot(const T* __restrict__ pc, int64_t ld, int
   for (; c < c1; ++c) a[0] = fma(ldg_stream(pc + (int64_t)c * ld), buf[c], a[0]);
 }
 
-// five resident CTAs per SM (48 registers, no spills): C3-sized blocks
-// 0.278 -> 0.245 ms per local solve over the unbounded 60 registers / four
-// CTAs; six (40 registers) and eight (32) spill and measured slower
-template <typename T, typename TI>
-__global__ void __launch_bounds__(CF_THREADS, 5) k_cf_dataflow(CoarseFactorDev F, CfSched S,
+// register cap from the resident-CTA target (256 threads: 5 per SM at 48
+// registers took C3-sized blocks 0.278 -> 0.245 ms; 6 and 8 spilled, slower)
+template <typename T, typename TI, int CF_THREADS>
+__global__ void __launch_bounds__(CF_THREADS, cf_min_ctas(CF_THREADS)) k_cf_dataflow(CoarseFactorDev F, CfSched S,
                                                             const int2* __restrict__ tasks,
                                                             const T* __restrict__ vals, const TI* __restrict__ u,
                                                             const int32_t* __restrict__ gmap, T* __restrict__ y,

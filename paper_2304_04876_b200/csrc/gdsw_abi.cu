@@ -585,6 +585,7 @@ struct FactorBuf {
   DBuf<int32_t> parent, child_ptr, child_idx, fwd_need, bwd_need, ready;
   DBuf<unsigned> ticket;
   int32_t n_fwd_tasks = 0, n_df_tasks = 0, n_sn = 0, df_grid = 0;
+  int nt = CF_NT_COARSE;                  // dataflow CTA size (coarse_factor.cuh)
   size_t df_smem = 0;
   DBuf<char> vals, ybuf, cbuf, fcm;
   DBuf<int64_t> f_off;
@@ -899,8 +900,12 @@ void factor_solve(const FactorBuf& F, const TI* u, const int32_t* gmap, T* x, cu
   const CoarseFactorDev D = F.dev();
   // one launch: dependency-driven tiles (k_cf_dataflow)
   CfSched S{F.ticket.p, F.ready.p, F.ready.p + F.n_sn, F.n_fwd_tasks, F.n_df_tasks, F.n_sn};
-  k_cf_dataflow<T, TI><<<F.df_grid, CF_THREADS, F.df_smem, s>>>(D, S, F.df_tasks.p, (const T*)F.vals.p, u, gmap,
-                                                                 (T*)F.ybuf.p, (T*)F.cbuf.p, x, (const T*)F.fcm.p);
+  if (F.nt == CF_NT_LOCAL)
+    k_cf_dataflow<T, TI, CF_NT_LOCAL><<<F.df_grid, CF_NT_LOCAL, F.df_smem, s>>>(
+        D, S, F.df_tasks.p, (const T*)F.vals.p, u, gmap, (T*)F.ybuf.p, (T*)F.cbuf.p, x, (const T*)F.fcm.p);
+  else
+    k_cf_dataflow<T, TI, CF_NT_COARSE><<<F.df_grid, CF_NT_COARSE, F.df_smem, s>>>(
+        D, S, F.df_tasks.p, (const T*)F.vals.p, u, gmap, (T*)F.ybuf.p, (T*)F.cbuf.p, x, (const T*)F.fcm.p);
   CK_LAUNCH();
 }
 
@@ -1559,7 +1564,22 @@ extern "C" {
 // upload a host partitioned inverse (gdsw_coarse_factor) into F in the
 // precond dtype; tasks are CF_ROWS-row tiles of each supernode's stacked
 // rows (forward: s + r, backward: s)
-static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype, size_t es, int64_t cm_default) {
+// resident CTAs per SM of the dataflow kernel at CTA size nt
+static int cf_occupancy(bool f32, int nt, size_t smem) {
+  int occ = 0;
+  if (nt == CF_NT_LOCAL) {
+    if (f32) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cf_dataflow<float, double, CF_NT_LOCAL>, nt, smem));
+    else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cf_dataflow<double, double, CF_NT_LOCAL>, nt, smem));
+  } else {
+    if (f32) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cf_dataflow<float, double, CF_NT_COARSE>, nt, smem));
+    else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cf_dataflow<double, double, CF_NT_COARSE>, nt, smem));
+  }
+  return occ;
+}
+
+static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype, size_t es, int64_t cm_default,
+                           int nt = CF_NT_COARSE) {
+  F.nt = nt;
   const int nsn = f->n_sn, nl = f->n_levels;
   auto i32 = [](const int64_t* a, size_t n) { return to_i32(a, n); };
   F.sn_s.upload(i32(f->sn_s, nsn));
@@ -1610,21 +1630,21 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
   require(smax <= 200 * 1024, "partitioned-inverse supernode too large for shared memory");
   if (smax > 48 * 1024) {  // before the occupancy query below
     auto big = [&](auto kern) { CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax)); };
-    big(k_cf_dataflow<double, double>);
-    big(k_cf_dataflow<float, double>);
-    big(k_cf_dataflow<float, float>);
+    big(k_cf_dataflow<double, double, CF_NT_LOCAL>);
+    big(k_cf_dataflow<float, double, CF_NT_LOCAL>);
+    big(k_cf_dataflow<float, float, CF_NT_LOCAL>);
+    big(k_cf_dataflow<double, double, CF_NT_COARSE>);
+    big(k_cf_dataflow<float, double, CF_NT_COARSE>);
+    big(k_cf_dataflow<float, float, CF_NT_COARSE>);
   }
   // dataflow schedule: forward tiles leaves-first, backward tiles root-first;
   // parent = supernode of the first row below, readiness targets in tiles.
   // Tile rows per level and direction: about one tile per resident CTA
   // slot (GDSW_CF_TPS; measured 1 < 2 < 4 with the column-major panels: C3-
-  // sized blocks 0.28 / 0.30 / 0.40 ms), clamped to 8..128 rows
+  // sized blocks 0.28 / 0.30 / 0.40 ms), clamped to 8..nt/2 rows
   {
     int occ = 0;
-    if (dtype == GDSW_F32)
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cf_dataflow<float, double>, CF_THREADS, smax));
-    else
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cf_dataflow<double, double>, CF_THREADS, smax));
+    occ = cf_occupancy(dtype == GDSW_F32, F.nt, smax);
     const int64_t slots = (int64_t)num_sms() * std::max(occ, 1);
     std::vector<int32_t> tile_f(nl), tile_b(nl);
     for (int l = 0; l < nl; ++l) {
@@ -1639,7 +1659,7 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
       }();
       auto pick = [&](int64_t rows) {
         int64_t t = (rows + tps * slots - 1) / (tps * slots);
-        t = std::min<int64_t>(128, std::max<int64_t>(CF_ROWS, (t + 7) / 8 * 8));
+        t = std::min<int64_t>(F.nt / 2, std::max<int64_t>(CF_ROWS, (t + 7) / 8 * 8));
         return (int32_t)t;
       };
       tile_f[l] = pick(rf);
@@ -1709,8 +1729,7 @@ static void install_factor(FactorBuf& F, const gdsw_coarse_factor* f, int dtype,
     F.ybuf.alloc((size_t)f->n * sizeof(T));
     F.cbuf.alloc((size_t)std::max<int64_t>(nrow, 1) * sizeof(T));
     // persistent grid: every CTA resident
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cf_dataflow<T, double>, CF_THREADS, smax));
+    const int occ = cf_occupancy(sizeof(T) == 4, F.nt, smax);
     F.df_grid = std::max(1, std::min(F.n_df_tasks, num_sms() * std::max(occ, 1)));
   });
   F.on = true;
@@ -1791,7 +1810,10 @@ int gdsw_precond_set_local_factor(gdsw_precond* m, const gdsw_coarse_factor* f) 
     if (f == nullptr) {
       m->lf = FactorBuf{};
     } else {
-      install_factor(m->lf, f, m->dtype, m->es, CF_CM_LOCAL);
+      // 128-thread CTAs when the blocks outnumber the SMs (C3: 92.4 -> 87.8
+      // ms); few blocks keep 256 (C1 4.4 vs 4.56 ms)
+      install_factor(m->lf, f, m->dtype, m->es, CF_CM_LOCAL,
+                     m->plan->n_sub > num_sms() ? CF_NT_LOCAL : CF_NT_COARSE);
       if (!f->values)
         with_dtype(m->dtype, [&](auto tag) { pinv_device_build<decltype(tag)>(m, m->lf, f); });
     }

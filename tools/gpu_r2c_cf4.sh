@@ -1,0 +1,9 @@
+# verify 128-thread dataflow kernel: exact-LU / coarse-factor parity, configs
+mkdir -p gpurun_out/cf4
+timeout 300 python tools/profile_ts.py C3s 20 2>&1 | tail -1; timeout 300 python tools/profile_ts.py C1 50 2>&1 | tail -1
+timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_configs.py tests/test_coarse_factor.py tests/test_gpu_acceptance.py tests/test_gpu_dist.py -m gpu -q -x > gpurun_out/cf4/pytest.log 2>&1; tail -1 gpurun_out/cf4/pytest.log
+timeout 1500 python tools/run_configs.py C1 C3 C5_2048 > gpurun_out/cf4/configs.jsonl 2> gpurun_out/cf4/configs.err
+python -c "
+import json
+for l in open('gpurun_out/cf4/configs.jsonl'):
+    d=json.loads(l); print(d['config'], d['iterations'], round(d['solve_ms'],2), round(d['ms_per_iteration'],3), round(d['apply_ms'],3))"
