@@ -20,14 +20,14 @@
 namespace gdsw {
 
 // CTA shapes of the dataflow kernel (48 registers either way): local exact-LU
-// blocks that outnumber the SMs run 128 threads x 10 resident CTAs (C3-sized
+// solves of 32+ blocks run 128 threads x 10 resident CTAs (C3-sized
 // blocks 0.245 -> 0.220 ms, C3 92.4 -> 87.8 ms), the coarse factor and few
 // blocks 256 x 5 (128 threads measured slower there: n_c = 12,600, C5 2,048
 // subdomains 41.6 -> 44.9 ms; C1 4.4 -> 4.56 ms). A narrow
 // tile (thread per row, columns split in at least two parts) holds at most
 // NT / 2 rows: the host tiler clamps to that.
 constexpr int CF_NT_LOCAL = 128, CF_NT_COARSE = 256;
-constexpr int cf_min_ctas(int nt) { return nt == 128 ? 10 : 5; }
+constexpr int cf_min_ctas(int nt) { return 1280 / nt; }  // 10 x 128, 5 x 256 (48 registers)
 constexpr int CF_ROWS = 8;   // smallest tile: one row per warp
 
 struct CoarseFactorDev {

@@ -1810,10 +1810,11 @@ int gdsw_precond_set_local_factor(gdsw_precond* m, const gdsw_coarse_factor* f) 
     if (f == nullptr) {
       m->lf = FactorBuf{};
     } else {
-      // 128-thread CTAs when the blocks outnumber the SMs (C3: 92.4 -> 87.8
-      // ms); few blocks keep 256 (C1 4.4 vs 4.56 ms)
+      // 128-thread CTAs from 32 blocks up (C3 512 blocks: 92.4 -> 87.8 ms;
+      // 64 C3-sized blocks 0.245 -> 0.220 ms); few blocks keep 256 (C1, 8
+      // blocks: 4.4 vs 4.56 ms)
       install_factor(m->lf, f, m->dtype, m->es, CF_CM_LOCAL,
-                     m->plan->n_sub > num_sms() ? CF_NT_LOCAL : CF_NT_COARSE);
+                     m->plan->n_sub >= 32 ? CF_NT_LOCAL : CF_NT_COARSE);
       if (!f->values)
         with_dtype(m->dtype, [&](auto tag) { pinv_device_build<decltype(tag)>(m, m->lf, f); });
     }
